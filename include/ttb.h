@@ -1,0 +1,144 @@
+/*
+ * ttb.h -- C ABI of the B200-native TT-rounding library (libttb, built as
+ * paper_2011_06532_b200/_ttb.so).
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json:
+ * TT-rounding with its Gram-sweep (inner product / norm), orthonormalization,
+ * and the add / Hadamard constructors.  Every entry point replaces one call
+ * of the reference package `ttpar` (pure Python + scipy LAPACK); the
+ * reference interface each one stands in for is cited beside it
+ * (paths relative to /root/reference/pkg/src/ttpar/).
+ *
+ * Conventions
+ *  - Plain C types only: device pointers as `double*`, sizes as int64_t,
+ *    CUDA streams as `void*` (a cudaStream_t).  No torch types.
+ *  - A TT "slab set" is ndim device arrays; core n is the LOCAL block of
+ *    mode-n slices owned by this rank, Fortran-ordered with shape
+ *    (ranks[n], dims[n], ranks[n+1]) -- the reference's natural descending
+ *    layout (core.py:1-23) restricted to block_bounds rows (parallel.py:42-46).
+ *  - Inputs are never modified (value semantics, parallel.py:315, ops.py:74).
+ *    Outputs are caller-allocated; for rank-reducing calls they are sized by
+ *    the INPUT ranks and the kernels write the (smaller) result packed at
+ *    the front of each buffer, reporting the actual ranks.
+ *  - Every function returns TTB_OK (0) or an error code; the message is in
+ *    ttb_last_error().  Codes map 1:1 onto the reference's exception classes
+ *    (errors.py:4-33).  Calls are asynchronous on the context stream unless
+ *    they return a host value (then they synchronize that stream).
+ *  - Multi-GPU: one process per GPU.  Call ttb_ctx_init_comm on every rank
+ *    with the same 128-byte NCCL unique id; all collective calls must then
+ *    be made by every rank in the same order (the reference's SPMD contract,
+ *    comm.py:134-160).  Not thread-safe per context.
+ */
+#ifndef TTB_H_
+#define TTB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTB_ABI_VERSION 1
+
+enum {
+  TTB_OK = 0,
+  TTB_ERR_SHAPE = 1,      /* ttpar.errors.ShapeError      */
+  TTB_ERR_CONTRACT = 2,   /* ttpar.errors.ContractError   */
+  TTB_ERR_NUMERIC = 3,    /* ttpar.errors.NumericError    */
+  TTB_ERR_CAPACITY = 4,   /* ttpar.errors.CapacityError   */
+  TTB_ERR_CUDA = 5,       /* CUDA runtime failure          */
+  TTB_ERR_NCCL = 6,       /* NCCL failure                  */
+  TTB_ERR_CAPABILITY = 7  /* ttpar.errors.CapabilityError */
+};
+
+typedef struct ttb_ctx ttb_ctx;
+typedef struct ttb_tsqr ttb_tsqr;
+
+/* ---- library / context ------------------------------------------------ */
+const char* ttb_last_error(void);
+int ttb_abi_version(void);
+/* number of kernels this library has launched in the process (evidence) */
+long long ttb_launch_counter(void);
+
+/* One context per (process, device).  Replaces the Communicator endpoint
+ * (comm.py:134-160; SerialComm comm.py:163-181). */
+int ttb_ctx_create(int device, void* stream, ttb_ctx** out);
+int ttb_ctx_destroy(ttb_ctx* ctx);
+int ttb_ctx_set_stream(ttb_ctx* ctx, void* stream);
+/* NCCL bootstrap: rank 0 creates the id, the host broadcasts it
+ * (replaces MPICommunicator, comm.py:359-401). */
+int ttb_comm_unique_id(void* out128);
+int ttb_ctx_init_comm(ttb_ctx* ctx, int nranks, int rank, const void* id128);
+
+/* ---- construction (no communication) ---------------------------------- */
+/* out = s * x elementwise over n doubles (scale folds into core 0,
+ * ops.py:71-76). */
+int ttb_scale(ttb_ctx* ctx, int64_t n, const double* x, double s, double* out);
+
+/* N-ary block-diagonal sum  sum_p scales[p] * X_p  (ops.py:79-106, with
+ * scale ops.py:71-76 fused: the scale multiplies core 0 only).
+ * ranks: nterms rows of (ndim+1); cores: nterms rows of ndim pointers;
+ * out[n] has shape (sum_p ranks[p][n] (1 at n=0), dims[n],
+ * sum_p ranks[p][n+1] (1 at n=ndim-1)).  ndim == 1 sums elementwise. */
+int ttb_add(ttb_ctx* ctx, int nterms, int ndim, const int64_t* dims, const int64_t* ranks,
+            const double* const* cores, const double* scales, double* const* out);
+
+/* Slice-wise Kronecker product (ops.py:109-132): out[n] has shape
+ * (rx[n]*ry[n], dims[n], rx[n+1]*ry[n+1]), x's rank index slow. */
+int ttb_hadamard(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
+                 const double* const* x, const double* const* y, double* const* out);
+
+/* ---- Gram sweeps ------------------------------------------------------ */
+/* <x, y> (ops.py:135-155): W_n = sum_i Y_n(i)^T W_{n-1} X_n(i), allreduced
+ * per mode.  *result is written on the host. */
+int ttb_inner(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
+              const double* const* x, const double* const* y, double* result);
+
+/* sum of squares of n doubles, allreduced (parallel.py:362-365, ops.py:232-234) */
+int ttb_sumsq(ttb_ctx* ctx, int64_t n, const double* x, double* result);
+
+/* ---- orthonormalization / rounding ------------------------------------ */
+/* Alg. 3 sweep (parallel.py:164-209). direction 0 = left, 1 = right.
+ * out[n] has the input shapes. */
+int ttb_orthonormalize(ttb_ctx* ctx, int direction, int ndim, const int64_t* dims,
+                       const int64_t* ranks, const double* const* in, double* const* out);
+
+/* round_tt (parallel.py:293-438) with RoundingOptions (parallel.py:261-284).
+ * variant: 0 LRLI, 1 LRL, 2 RLRI, 3 RLR.  max_rank <= 0 means no cap.
+ * out[n] sized by the input ranks; results packed at the front with shape
+ * (out_ranks[n], dims[n], out_ranks[n+1]).  meta[0..3] = norm, eps_bond,
+ * error_bound_violated (0/1), zero (0/1) -- the reference's meta dict. */
+int ttb_round(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim,
+              const int64_t* dims, const int64_t* ranks, const double* const* in,
+              double* const* out, int64_t* out_ranks, double* meta);
+
+/* ---- building blocks (the reference's lower-level public API) --------- */
+/* TSQR of the panel view of one slab (rl, I, rr): trans 0 -> V(X) (rows
+ * r_left*I, cols rr), trans 1 -> H(X)^T (rows I*rr, cols rl).  A plain
+ * column-major m x b matrix is the slab (1, m, b) with trans 0.
+ * Replaces tsqr_factor (tsqr.py:166-221); r_out (device, b x b col-major)
+ * receives the replicated, sign-fixed R (tsqr.py:127-129). */
+int ttb_tsqr_factor(ttb_ctx* ctx, int64_t rl, int64_t I, int64_t rr, int trans, const double* slab,
+                    ttb_tsqr** out, double* r_out);
+/* out = rows of Q @ [c; 0] on this rank (tsqr_apply_q, tsqr.py:248-327):
+ * c is b x k (device, col-major), out is the slab (rl, I, k) for trans 0 or
+ * (k, I, rr) for trans 1. */
+int ttb_tsqr_apply(ttb_ctx* ctx, const ttb_tsqr* f, int64_t k, const double* c, double* out);
+int ttb_tsqr_free(ttb_ctx* ctx, ttb_tsqr* f);
+
+/* truncated_svd (parallel.py:224-258) of an m x n device matrix (col-major,
+ * m, n <= 64): one-sided Jacobi on the device.  u (m x min), s (min),
+ * v (n x min) are written for the first *keep columns. */
+int ttb_truncated_svd(ttb_ctx* ctx, int64_t m, int64_t n, const double* a, double eps,
+                      int64_t max_rank, double* u, double* s, double* v, int64_t* keep,
+                      double* tail, int* capped);
+
+/* measured fp64 throughput of this device (TFLOP/s): scalar DFMA and
+ * warp-level DMMA (mma.sync m8n8k4 f64).  Roofline denominators. */
+int ttb_fp64_peak(void* stream, double* dfma_tflops, double* dmma_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTB_H_ */

@@ -1,0 +1,170 @@
+"""Device-group endpoints: the B200 stand-in for ttpar's Communicator
+(comm.py:134-160).
+
+One process drives one GPU (torch.distributed launches the ranks).  The
+communicator owns the native context (stream binding, NCCL communicator for
+the in-kernel-path collectives: the TSQR R allgather and the Gram / norm
+allreduces) and offers the host-side collectives the harness needs
+(gather of slabs, object exchange) through torch.distributed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import CapabilityError, ContractError
+
+
+class Communicator:
+    """Endpoint of a P-rank device group.  ``size``/``rank`` as in ttpar."""
+
+    size = 1
+    rank = 0
+
+    def __init__(self, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise CapabilityError("no CUDA device: the B200 path has no CPU fallback")
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise CapabilityError("communicator device must be a CUDA device")
+        self._ctx = None
+        self.trace = _NullTrace()
+
+    # -- native context ------------------------------------------------------
+    def ctx(self):
+        """Native context handle bound to the current torch stream."""
+        import torch
+
+        lib = _lib.load()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        if self._ctx is None:
+            h = C.c_void_p()
+            with torch.cuda.device(self.device):
+                _lib.check(lib.ttb_ctx_create(self.device.index, C.c_void_p(stream), C.byref(h)))
+            self._ctx = h
+            self._init_comm()
+        else:
+            _lib.check(lib.ttb_ctx_set_stream(self._ctx, C.c_void_p(stream)))
+        return self._ctx
+
+    def _init_comm(self):
+        _lib.check(_lib.load().ttb_ctx_init_comm(self._ctx, 1, 0, None))
+
+    def close(self):
+        if self._ctx is not None:
+            _lib.load().ttb_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- host-side collectives (harness / gather) ----------------------------
+    def allreduce_sum(self, arr):
+        return np.asarray(arr, dtype=np.float64).copy()
+
+    def allgather_object(self, obj):
+        return [obj]
+
+    def barrier(self):
+        pass
+
+
+class SerialComm(Communicator):
+    """One-rank group on the current device (ttpar SerialComm, comm.py:163-181)."""
+
+
+class DistComm(Communicator):
+    """Rank of a torch.distributed process group, one GPU per process.
+
+    The NCCL communicator the native collectives use is bootstrapped with a
+    unique id created on rank 0 and broadcast over the torch group.
+    """
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ContractError("DistComm needs an initialised torch.distributed process group")
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        super().__init__(device)
+
+    def _init_comm(self):
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        if self.size == 1:
+            _lib.check(lib.ttb_ctx_init_comm(self._ctx, 1, 0, None))
+            return
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(lib.ttb_comm_unique_id(uid))
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0, group=self.group)
+        uid = C.create_string_buffer(box[0], 128)
+        _lib.check(lib.ttb_ctx_init_comm(self._ctx, self.size, self.rank, uid))
+
+    def allreduce_sum(self, arr):
+        import torch
+        import torch.distributed as dist
+
+        a = np.asarray(arr, dtype=np.float64)
+        parts = self.allgather_object(a)
+        out = np.zeros_like(a)
+        for p in parts:  # rank-ascending, deterministic (comm.py:220-225)
+            out = out + p
+        return out
+
+    def allgather_object(self, obj):
+        import torch.distributed as dist
+
+        box = [None] * self.size
+        dist.all_gather_object(box, obj, group=self.group)
+        return box
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+
+class _NullTrace:
+    """Placeholder for ttpar's Trace: phase timing lives in the native layer."""
+
+    def reset(self):
+        pass
+
+    def total(self, key):
+        return 0.0
+
+    def add_flops(self, f):
+        pass
+
+
+_default = {}
+
+
+def default_comm():
+    """Process-wide SerialComm on the current CUDA device."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise CapabilityError("no CUDA device: the B200 path has no CPU fallback")
+    dev = torch.cuda.current_device()
+    if dev not in _default:
+        _default[dev] = SerialComm(torch.device("cuda", dev))
+    return _default[dev]

@@ -1,0 +1,166 @@
+// Context, error plumbing, NCCL (dlopen) and the context C-ABI entry points.
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "ctx.cuh"
+
+namespace ttb {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+// ---- NCCL through dlopen -------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void* id) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+
+struct UniqueId { char internal[128]; };
+typedef int (*commInitRank_byval_t)(void** comm, int nranks, UniqueId id, int rank);
+
+static NcclApi g_nccl;
+static commInitRank_byval_t g_commInitRank = nullptr;
+static std::mutex g_nccl_mu;
+
+static void load_nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.h) return;
+  const char* env = getenv("TTB_NCCL_LIB");
+  const char* cands[] = {env, "libnccl.so.2", "libnccl.so"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    g_nccl.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  TTB_CHECK(g_nccl.h, TTB_ERR_NCCL, "could not dlopen libnccl.so.2 (set TTB_NCCL_LIB)");
+  g_nccl.getUniqueId = (int (*)(void*))dlsym(g_nccl.h, "ncclGetUniqueId");
+  g_commInitRank = (commInitRank_byval_t)dlsym(g_nccl.h, "ncclCommInitRank");
+  g_nccl.allGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclAllGather");
+  g_nccl.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclAllReduce");
+  g_nccl.commDestroy = (int (*)(void*))dlsym(g_nccl.h, "ncclCommDestroy");
+  g_nccl.getErrorString = (const char* (*)(int))dlsym(g_nccl.h, "ncclGetErrorString");
+  TTB_CHECK(g_nccl.getUniqueId && g_commInitRank && g_nccl.allGather && g_nccl.allReduce, TTB_ERR_NCCL,
+            "libnccl is missing required symbols");
+}
+
+static void nccl_check(int rc, const char* what) {
+  if (rc != 0) {
+    std::string msg = std::string(what) + " failed";
+    if (g_nccl.getErrorString) msg += std::string(": ") + g_nccl.getErrorString(rc);
+    TTB_THROW(TTB_ERR_NCCL, msg);
+  }
+}
+
+static constexpr int kNcclDouble = 8;  // ncclFloat64
+static constexpr int kNcclSum = 0;     // ncclSum
+
+void* Ctx::alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 256;
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    TTB_THROW(TTB_ERR_CAPACITY, std::string("device allocation of ") + std::to_string(bytes) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void Ctx::free(void* p) {
+  if (p) TTB_CUDA(cudaFreeAsync(p, stream));
+}
+
+void Ctx::allgather(const double* send, double* recv, size_t count) {
+  TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
+  nccl_check(g_nccl.allGather(send, recv, count, kNcclDouble, nccl_comm, stream), "ncclAllGather");
+}
+
+void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
+  TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
+  nccl_check(g_nccl.allReduce(send, recv, count, kNcclDouble, kNcclSum, nccl_comm, stream), "ncclAllReduce");
+}
+
+void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }
+
+}  // namespace ttb
+
+using namespace ttb;
+
+extern "C" {
+
+const char* ttb_last_error(void) { return g_last_error.c_str(); }
+
+int ttb_abi_version(void) { return TTB_ABI_VERSION; }
+
+long long ttb_launch_counter(void) { return g_launches.load(); }
+
+int ttb_ctx_create(int device, void* stream, ttb_ctx** out) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(out, TTB_ERR_CONTRACT, "null output pointer");
+  TTB_CUDA(cudaSetDevice(device));
+  ttb_ctx* c = new ttb_ctx();
+  c->c.device = device;
+  c->c.stream = (cudaStream_t)stream;
+  TTB_CUDA(cudaDeviceGetAttribute(&c->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+  int cc_major = 0, cc_minor = 0;
+  TTB_CUDA(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  TTB_CUDA(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (cc_major != 10 || cc_minor != 0) {
+    delete c;
+    TTB_THROW(TTB_ERR_CAPABILITY, "this build targets sm_100a (B200); device is sm_" +
+                                      std::to_string(cc_major) + std::to_string(cc_minor));
+  }
+  *out = c;
+  TTB_TRY_END
+}
+
+int ttb_ctx_destroy(ttb_ctx* ctx) {
+  TTB_TRY_BEGIN
+  if (ctx) {
+    if (ctx->c.nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->c.nccl_comm);
+    delete ctx;
+  }
+  TTB_TRY_END
+}
+
+int ttb_ctx_set_stream(ttb_ctx* ctx, void* stream) {
+  TTB_TRY_BEGIN
+  ctx->c.stream = (cudaStream_t)stream;
+  TTB_TRY_END
+}
+
+int ttb_comm_unique_id(void* out128) {
+  TTB_TRY_BEGIN
+  load_nccl();
+  nccl_check(g_nccl.getUniqueId(out128), "ncclGetUniqueId");
+  TTB_TRY_END
+}
+
+int ttb_ctx_init_comm(ttb_ctx* ctx, int nranks, int rank, const void* id128) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, TTB_ERR_CONTRACT, "bad rank/size");
+  ctx->c.nranks = nranks;
+  ctx->c.rank = rank;
+  if (nranks > 1) {
+    load_nccl();
+    TTB_CUDA(cudaSetDevice(ctx->c.device));
+    UniqueId id;
+    memcpy(id.internal, id128, 128);
+    void* comm = nullptr;
+    nccl_check(g_commInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+    ctx->c.nccl_comm = comm;
+  }
+  TTB_TRY_END
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// Per-device execution context: stream, SM count, stream-ordered workspace
+// allocation, and the (optional) NCCL communicator used by the multi-GPU
+// paths.  NCCL is resolved at run time with dlopen so the library does not
+// pin a second libnccl next to the one torch loads.
+#pragma once
+
+#include "common.cuh"
+#include "tsqr.cuh"
+
+namespace ttb {
+
+struct NcclApi;  // defined in ctx.cu
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int nranks = 1;
+  int rank = 0;
+  void* nccl_comm = nullptr;
+  cudaEvent_t ev = nullptr;
+
+  void* alloc(size_t bytes);
+  void free(void* p);
+  // collectives on this->stream (nranks > 1 only)
+  void allgather(const double* send, double* recv, size_t count);
+  void allreduce_sum(const double* send, double* recv, size_t count);
+  void sync();
+};
+
+// host-side TSQR factor object (see tsqr.cu)
+struct Tsqr {
+  int b = 0, cls = 0;
+  Panel panel;
+  LeafPlan plan;
+  int ldy = 0, ldy_tree = 0, ftree = 0;
+  double *Y = nullptr, *T = nullptr, *Rleaf = nullptr;
+  int nloc = 0, nglob = 0;
+  double *locY[kMaxLevels], *locT[kMaxLevels], *locR[kMaxLevels];
+  double *gloY[kMaxLevels], *gloT[kMaxLevels], *gloR[kMaxLevels];
+  double* Rstack = nullptr;
+  const double* Rlocal = nullptr;
+  const double* Rraw = nullptr;
+  double* D = nullptr;  // sign fix (b)
+  double* R = nullptr;  // final sign-fixed R (b x b, col-major), replicated
+  void* mem = nullptr;
+};
+
+int tsqr_class(int b);
+void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f);
+// out (view with k columns, same slicing as the factored panel) = Q [D z; 0]
+void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& out);
+void tsqr_release(Ctx& ctx, Tsqr& f);
+
+}  // namespace ttb
+
+struct ttb_ctx {
+  ttb::Ctx c;
+};

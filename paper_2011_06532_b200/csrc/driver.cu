@@ -1,0 +1,430 @@
+// Native drivers behind the C ABI (include/ttb.h): TT construction, Gram
+// sweeps, orthonormalization and the four rounding variants.  These replace
+// the reference's Python sweep loops (parallel.py:164-209, 293-438;
+// ops.py:71-155) with a host loop that only enqueues kernels on the context
+// stream; the single host sync per truncation step reads back the kept rank.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ops.cuh"
+#include "svd.cuh"
+
+struct ttb_tsqr {
+  ttb::Tsqr f;
+};
+
+namespace ttb {
+
+__global__ void eye_kernel(double* e, int b) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < b * b; idx += blockDim.x * gridDim.x)
+    e[idx] = (idx % b == idx / b) ? 1.0 : 0.0;
+}
+
+static double* make_eye(Ctx& ctx, int b) {
+  double* e = (double*)ctx.alloc((size_t)b * b * sizeof(double));
+  eye_kernel<<<1, 256, 0, ctx.stream>>>(e, b);
+  TTB_LAUNCHED();
+  return e;
+}
+
+static void copy_d2d(Ctx& ctx, double* dst, const double* src, int64_t n) {
+  if (n > 0) TTB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+static Panel panel_of(const double* p, int64_t rl, int64_t I, int64_t rr, int trans) {
+  Panel q;
+  q.base = const_cast<double*>(p);
+  q.rl = rl;
+  q.I = I;
+  q.rr = rr;
+  q.trans = trans;
+  return q;
+}
+
+static void check_chain(int ndim, const int64_t* dims, const int64_t* ranks) {
+  TTB_CHECK(ndim >= 1, TTB_ERR_SHAPE, "a TT tensor needs at least one core");
+  TTB_CHECK(ranks[0] == 1 && ranks[ndim] == 1, TTB_ERR_SHAPE, "end ranks must be 1");
+  for (int n = 0; n < ndim; ++n) {
+    TTB_CHECK(dims[n] >= 0, TTB_ERR_SHAPE, "local mode sizes must be >= 0");
+    TTB_CHECK(ranks[n + 1] >= 1, TTB_ERR_SHAPE, "ranks must be positive");
+  }
+}
+
+static double host_scalar(Ctx& ctx, const double* d) {
+  double h = 0.0;
+  TTB_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  return h;
+}
+
+// sum of squares of a device vector, allreduced over ranks; returns host value
+static double global_sumsq(Ctx& ctx, int64_t n, const double* x) {
+  double* d = (double*)ctx.alloc(2 * sizeof(double));
+  if (n > 0) sumsq_dev(ctx, n, x, d);
+  else fill_zero(ctx, d, 1);
+  if (ctx.nranks > 1) ctx.allreduce_sum(d, d + 1, 1);
+  double v = host_scalar(ctx, ctx.nranks > 1 ? d + 1 : d);
+  ctx.free(d);
+  return v;
+}
+
+struct SvdOut {
+  double* C = nullptr;
+  double* Vk = nullptr;
+  double* s = nullptr;
+  int* info = nullptr;
+  double* dinfo = nullptr;
+  void* mem = nullptr;
+  int keep = 0, capped = 0;
+  double tail = 0.0;
+};
+
+// SVD of A = R^T (R the b x b TSQR factor), truncated; host learns keep
+static void svd_of_rt(Ctx& ctx, const double* R, int b, double eps, int max_rank, SvdOut& o) {
+  const size_t bb = (size_t)b * b;
+  o.mem = ctx.alloc((2 * bb + b + 1) * sizeof(double) + 4 * sizeof(int) + 64);
+  o.C = (double*)o.mem;
+  o.Vk = o.C + bb;
+  o.s = o.Vk + bb;
+  o.dinfo = o.s + b;
+  o.info = (int*)(o.dinfo + 1);
+  jacobi_svd(ctx, R, b, b, b, true, eps, max_rank, o.C, o.Vk, o.s, o.info, o.dinfo);
+  int hinfo[3] = {0, 0, 0};
+  TTB_CUDA(cudaMemcpyAsync(hinfo, o.info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  TTB_CHECK(hinfo[2] == 0, TTB_ERR_NUMERIC, "non-finite entries in SVD input");
+  o.keep = hinfo[0];
+  o.capped = hinfo[1];
+}
+
+}  // namespace ttb
+
+using namespace ttb;
+
+extern "C" {
+
+int ttb_scale(ttb_ctx* h, int64_t n, const double* x, double s, double* out) {
+  TTB_TRY_BEGIN
+  scale_vec(h->c, n, x, s, out);
+  TTB_TRY_END
+}
+
+int ttb_add(ttb_ctx* h, int nterms, int ndim, const int64_t* dims, const int64_t* ranks, const double* const* cores,
+            const double* scales, double* const* out) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  TTB_CHECK(nterms >= 1 && nterms <= kMaxAddTerms, TTB_ERR_CAPABILITY, "add: 1..16 terms");
+  for (int p = 0; p < nterms; ++p) check_chain(ndim, dims, ranks + (int64_t)p * (ndim + 1));
+  for (int n = 0; n < ndim; ++n) {
+    AddTerm t[kMaxAddTerms];
+    int64_t offa = 0, offc = 0;
+    for (int p = 0; p < nterms; ++p) {
+      const int64_t* rk = ranks + (int64_t)p * (ndim + 1);
+      t[p].x = cores[(int64_t)p * ndim + n];
+      t[p].rl = rk[n];
+      t[p].rr = rk[n + 1];
+      t[p].offa = offa;
+      t[p].offc = offc;
+      t[p].s = scales ? scales[p] : 1.0;
+      offa += rk[n];
+      offc += rk[n + 1];
+    }
+    int mode;
+    int64_t RL, RR;
+    if (ndim == 1) { mode = 3; RL = 1; RR = 1; }
+    else if (n == 0) { mode = 1; RL = 1; RR = offc; }
+    else if (n == ndim - 1) { mode = 2; RL = offa; RR = 1; }
+    else { mode = 0; RL = offa; RR = offc; }
+    add_core(ctx, mode, nterms, t, RL, dims[n], RR, out[n]);
+  }
+  TTB_TRY_END
+}
+
+int ttb_hadamard(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
+                 const double* const* x, const double* const* y, double* const* out) {
+  TTB_TRY_BEGIN
+  check_chain(ndim, dims, rx);
+  check_chain(ndim, dims, ry);
+  for (int n = 0; n < ndim; ++n) hadamard_core(h->c, x[n], rx[n], rx[n + 1], y[n], ry[n], ry[n + 1], dims[n], out[n]);
+  TTB_TRY_END
+}
+
+int ttb_inner(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
+              const double* const* x, const double* const* y, double* result) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, rx);
+  check_chain(ndim, dims, ry);
+  double* buf = (double*)ctx.alloc(3 * 64 * 64 * sizeof(double));
+  double* W = buf;
+  double* Wn = buf + 4096;
+  double* Wr = buf + 8192;
+  static const double one = 1.0;
+  TTB_CUDA(cudaMemcpyAsync(W, &one, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+  for (int n = 0; n < ndim; ++n) {
+    gram_step(ctx, W, x[n], rx[n], rx[n + 1], y[n], ry[n], ry[n + 1], dims[n], Wn);
+    if (ctx.nranks > 1) {
+      ctx.allreduce_sum(Wn, Wr, (size_t)(rx[n + 1] * ry[n + 1]));
+      std::swap(Wn, Wr);
+    }
+    std::swap(W, Wn);
+  }
+  *result = host_scalar(ctx, W);
+  ctx.free(buf);
+  TTB_TRY_END
+}
+
+int ttb_sumsq(ttb_ctx* h, int64_t n, const double* x, double* result) {
+  TTB_TRY_BEGIN
+  *result = global_sumsq(h->c, n, x);
+  TTB_TRY_END
+}
+
+int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims, const int64_t* ranks,
+                       const double* const* in, double* const* out) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, ranks);
+  TTB_CHECK(direction == 0 || direction == 1, TTB_ERR_CONTRACT, "direction must be 'left' or 'right'");
+  const int N = ndim;
+  if (N == 1) {
+    copy_d2d(ctx, out[0], in[0], ranks[0] * dims[0] * ranks[1]);
+    return TTB_OK;
+  }
+  if (direction == 0) {
+    const double* work = in[0];
+    for (int n = 0; n < N - 1; ++n) {
+      const int b = (int)ranks[n + 1];
+      Tsqr f;
+      tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 0), f);
+      double* eye = make_eye(ctx, b);
+      tsqr_apply(ctx, f, eye, b, panel_of(out[n], ranks[n], dims[n], b, 0));
+      gemm_small_left(ctx, b, b, dims[n + 1] * ranks[n + 2], f.R, b, false, in[n + 1], out[n + 1]);
+      ctx.free(eye);
+      tsqr_release(ctx, f);
+      work = out[n + 1];
+    }
+  } else {
+    const double* work = in[N - 1];
+    for (int n = N - 1; n >= 1; --n) {
+      const int b = (int)ranks[n];
+      Tsqr f;
+      tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 1), f);
+      double* eye = make_eye(ctx, b);
+      tsqr_apply(ctx, f, eye, b, panel_of(out[n], b, dims[n], ranks[n + 1], 1));
+      gemm_small_right(ctx, ranks[n - 1] * dims[n - 1], b, b, in[n - 1], f.R, b, true, out[n - 1]);
+      ctx.free(eye);
+      tsqr_release(ctx, f);
+      work = out[n - 1];
+    }
+  }
+  TTB_TRY_END
+}
+
+int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
+              const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks, double* meta) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, ranks);
+  TTB_CHECK(variant >= 0 && variant <= 3, TTB_ERR_CONTRACT, "unknown rounding variant");
+  TTB_CHECK(eps0 >= 0.0, TTB_ERR_CONTRACT, "eps0 must be nonnegative");
+  const int N = ndim;
+  const bool implicit = (variant == 0 || variant == 2);
+  const bool left_first = (variant == 0 || variant == 1);
+  std::vector<int64_t> r(ranks, ranks + N + 1);
+  std::vector<int64_t> d(dims, dims + N);
+  meta[0] = NAN;  // norm
+  meta[1] = NAN;  // eps_bond
+  meta[2] = 0.0;  // error_bound_violated
+  meta[3] = 0.0;  // zero
+  if (N == 1) {
+    copy_d2d(ctx, out[0], in[0], r[0] * d[0] * r[1]);
+    for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
+    return TTB_OK;
+  }
+  const int mr = max_rank > 0 ? (int)std::min<int64_t>(max_rank, 1 << 30) : 0;
+  std::vector<Tsqr> facs(N);
+  int64_t maxcore = 0;
+  for (int n = 0; n < N; ++n) maxcore = std::max(maxcore, r[n] * d[n] * r[n + 1]);
+  double* scratch = implicit ? nullptr : (double*)ctx.alloc((size_t)std::max<int64_t>(maxcore, 1) * sizeof(double));
+
+  // ---- orthonormalization sweep (implicit Q kept for *I variants) ----
+  const double* last = nullptr;
+  int64_t last_n = 0;
+  if (left_first) {
+    for (int n = 0; n < N - 1; ++n) {
+      const double* src = (n == 0) ? in[0] : out[n];
+      const int b = (int)r[n + 1];
+      tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 0), facs[n]);
+      if (!implicit) {
+        double* eye = make_eye(ctx, b);
+        tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], r[n], d[n], b, 0));
+        ctx.free(eye);
+      }
+      gemm_small_left(ctx, b, b, d[n + 1] * r[n + 2], facs[n].R, b, false, in[n + 1], out[n + 1]);
+      if (!implicit) tsqr_release(ctx, facs[n]);
+    }
+    last = out[N - 1];
+    last_n = r[N - 1] * d[N - 1] * r[N];
+  } else {
+    for (int n = N - 1; n >= 1; --n) {
+      const double* src = (n == N - 1) ? in[N - 1] : out[n];
+      const int b = (int)r[n];
+      tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 1), facs[n]);
+      if (!implicit) {
+        double* eye = make_eye(ctx, b);
+        tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], b, d[n], r[n + 1], 1));
+        ctx.free(eye);
+      }
+      gemm_small_right(ctx, r[n - 1] * d[n - 1], b, b, in[n - 1], facs[n].R, b, true, out[n - 1]);
+      if (!implicit) tsqr_release(ctx, facs[n]);
+    }
+    last = out[0];
+    last_n = r[0] * d[0] * r[1];
+  }
+
+  // ---- norm and per-bond threshold ----
+  const double nx = std::sqrt(std::max(global_sumsq(ctx, last_n, last), 0.0));
+  meta[0] = nx;
+  if (nx < 1e-300) {
+    for (int n = 0; n < N; ++n) {
+      if (implicit && facs[n].mem) tsqr_release(ctx, facs[n]);
+      fill_zero(ctx, out[n], d[n]);
+    }
+    for (int n = 0; n <= N; ++n) out_ranks[n] = 1;
+    meta[3] = 1.0;
+    if (scratch) ctx.free(scratch);
+    return TTB_OK;
+  }
+  const double eps = eps0 * nx / std::sqrt((double)(N - 1));
+  meta[1] = eps;
+
+  // ---- truncation sweep ----
+  bool violated = false;
+  if (left_first) {
+    for (int n = N - 1; n >= 1; --n) {
+      const int b = (int)r[n];
+      Tsqr f2;
+      tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2);
+      SvdOut so;
+      svd_of_rt(ctx, f2.R, b, eps, mr, so);
+      const int keep = so.keep;
+      violated |= so.capped != 0;
+      tsqr_apply(ctx, f2, so.Vk, keep, panel_of(out[n], keep, d[n], r[n + 1], 1));
+      if (implicit) {
+        tsqr_apply(ctx, facs[n - 1], so.C, keep, panel_of(out[n - 1], r[n - 1], d[n - 1], keep, 0));
+        tsqr_release(ctx, facs[n - 1]);
+      } else {
+        const int64_t Mb = r[n - 1] * d[n - 1];
+        gemm_small_right(ctx, Mb, b, keep, out[n - 1], so.C, b, false, scratch);
+        copy_d2d(ctx, out[n - 1], scratch, Mb * keep);
+      }
+      ctx.free(so.mem);
+      tsqr_release(ctx, f2);
+      r[n] = keep;
+    }
+  } else {
+    for (int n = 0; n < N - 1; ++n) {
+      const int b = (int)r[n + 1];
+      Tsqr f2;
+      tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 0), f2);
+      SvdOut so;
+      svd_of_rt(ctx, f2.R, b, eps, mr, so);
+      const int keep = so.keep;
+      violated |= so.capped != 0;
+      tsqr_apply(ctx, f2, so.Vk, keep, panel_of(out[n], r[n], d[n], keep, 0));
+      if (implicit) {
+        tsqr_apply(ctx, facs[n + 1], so.C, keep, panel_of(out[n + 1], keep, d[n + 1], r[n + 2], 1));
+        tsqr_release(ctx, facs[n + 1]);
+      } else {
+        const int64_t Nb = d[n + 1] * r[n + 2];
+        gemm_small_left(ctx, keep, b, Nb, so.C, b, true, out[n + 1], scratch);
+        copy_d2d(ctx, out[n + 1], scratch, keep * Nb);
+      }
+      ctx.free(so.mem);
+      tsqr_release(ctx, f2);
+      r[n + 1] = keep;
+    }
+  }
+  if (scratch) ctx.free(scratch);
+  meta[2] = violated ? 1.0 : 0.0;
+  for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
+  TTB_TRY_END
+}
+
+int ttb_tsqr_factor(ttb_ctx* h, int64_t rl, int64_t I, int64_t rr, int trans, const double* slab, ttb_tsqr** out,
+                    double* r_out) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  TTB_CHECK(out, TTB_ERR_CONTRACT, "null factor handle");
+  ttb_tsqr* f = new ttb_tsqr();
+  try {
+    tsqr_factor(ctx, panel_of(slab, rl, I, rr, trans ? 1 : 0), f->f);
+  } catch (...) {
+    delete f;
+    throw;
+  }
+  if (r_out) copy_d2d(ctx, r_out, f->f.R, (int64_t)f->f.b * f->f.b);
+  *out = f;
+  TTB_TRY_END
+}
+
+int ttb_tsqr_apply(ttb_ctx* h, const ttb_tsqr* f, int64_t k, const double* c, double* out) {
+  TTB_TRY_BEGIN
+  const Tsqr& F = f->f;
+  Panel o = F.panel;
+  o.base = out;
+  if (o.trans) o.rl = k;
+  else o.rr = k;
+  tsqr_apply(h->c, F, c, (int)k, o);
+  TTB_TRY_END
+}
+
+int ttb_tsqr_free(ttb_ctx* h, ttb_tsqr* f) {
+  TTB_TRY_BEGIN
+  if (f) {
+    tsqr_release(h->c, f->f);
+    delete f;
+  }
+  TTB_TRY_END
+}
+
+int ttb_truncated_svd(ttb_ctx* h, int64_t m, int64_t n, const double* a, double eps, int64_t max_rank, double* u,
+                      double* s, double* v, int64_t* keep, double* tail, int* capped) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  TTB_CHECK(m >= 1 && n >= 1 && m <= 64 && n <= 64, TTB_ERR_CAPABILITY, "truncated_svd: 1 <= m, n <= 64");
+  TTB_CHECK(eps >= 0.0, TTB_ERR_CONTRACT, "eps must be nonnegative");
+  const bool tall = m >= n;
+  const int M = (int)(tall ? m : n), Nn = (int)(tall ? n : m);
+  const size_t need = (size_t)(M * Nn + Nn * Nn + Nn + 1) * sizeof(double) + 4 * sizeof(int);
+  char* mem = (char*)ctx.alloc(need + 64);
+  double* C = (double*)mem;
+  double* Vk = C + (size_t)M * Nn;
+  double* sd = Vk + (size_t)Nn * Nn;
+  double* dinfo = sd + Nn;
+  int* info = (int*)(dinfo + 1);
+  jacobi_svd(ctx, a, (int)m, M, Nn, !tall, eps, max_rank > 0 ? (int)max_rank : 0, C, Vk, sd, info, dinfo);
+  int hinfo[3];
+  TTB_CUDA(cudaMemcpyAsync(hinfo, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  TTB_CUDA(cudaMemcpyAsync(tail, dinfo, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  TTB_CHECK(hinfo[2] == 0, TTB_ERR_NUMERIC, "non-finite entries in SVD input");
+  const int kp = hinfo[0];
+  *keep = kp;
+  *capped = hinfo[1];
+  copy_d2d(ctx, s, sd, kp);
+  if (tall) {  // A = (C/s) V^T
+    svd_normalize_u(ctx, C, sd, M, kp, u);
+    copy_d2d(ctx, v, Vk, (int64_t)Nn * kp);
+  } else {     // A^T = (C/s) Vk^T  =>  A = Vk s (C/s)^T
+    copy_d2d(ctx, u, Vk, (int64_t)Nn * kp);
+    svd_normalize_u(ctx, C, sd, M, kp, v);
+  }
+  ctx.sync();
+  ctx.free(mem);
+  TTB_TRY_END
+}
+
+}  // extern "C"

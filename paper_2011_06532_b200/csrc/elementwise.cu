@@ -1,0 +1,187 @@
+// Construction kernels: fused N-ary block-diagonal add with scales
+// (ops.py:71-106), slice-wise Kronecker Hadamard (ops.py:109-132), scale,
+// and a deterministic sum of squares (parallel.py:362-365).
+//
+// All are HBM-streaming kernels: each output element is written exactly once
+// with coalesced stores (a CTA owns one output column c and a run of slices,
+// i.e. a contiguous (a, i) range of the F-order core); inputs are read once
+// (add) or from L1/L2-resident slices (Hadamard).  Arithmetic is the exact
+// IEEE sequence of the reference (one multiply, left-to-right sums, no FMA
+// contraction) so results are bitwise identical to numpy.
+#include "ops.cuh"
+
+namespace ttb {
+
+constexpr int kEwNT = 256;
+constexpr int kEwElems = 4096;  // target output elements per CTA
+
+struct AddArgs {
+  int mode;  // 0 interior (block diagonal), 1 first core (concat along c), 2 last core (stack along a), 3 single core (sum)
+  int nterms;
+  AddTerm t[kMaxAddTerms];
+  int64_t RL, I, RR;
+  int ni;  // slices per CTA
+  double* out;
+};
+
+__global__ void __launch_bounds__(kEwNT) add_kernel(AddArgs a) {
+  const int64_t c = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * a.ni;
+  const int64_t ni = min64(a.ni, a.I - i0);
+  const int64_t RL = a.RL;
+  const int64_t cnt = RL * ni;
+  double* out = a.out + RL * (i0 + a.I * c);
+  if (a.mode == 3) {
+    for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
+      double acc = __dmul_rn(a.t[0].s, a.t[0].x[i0 + e]);
+      for (int p = 1; p < a.nterms; ++p) acc = __dadd_rn(acc, __dmul_rn(a.t[p].s, a.t[p].x[i0 + e]));
+      out[e] = acc;
+    }
+    return;
+  }
+  // term owning column c (modes 0, 1); for mode 2 the term is chosen per row
+  int pc = 0;
+  if (a.mode != 2) {
+    for (int p = 0; p < a.nterms; ++p)
+      if (c >= a.t[p].offc && c < a.t[p].offc + a.t[p].rr) pc = p;
+  }
+  const AddTerm T = a.t[pc];
+  if (a.mode == 1) {  // RL == 1: out(0, i, c) = s_p X_p(0, i, c - offc)
+    const double* x = T.x + (i0 + a.I * (c - T.offc));
+    for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) out[e] = __dmul_rn(T.s, x[e]);
+    return;
+  }
+  if (a.mode == 2) {  // RR == 1: out(a, i, 0) = X_p(a - offa, i, 0)
+    for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
+      const int64_t ai = e % RL, ii = e / RL;
+      int p = 0;
+      for (int q = 0; q < a.nterms; ++q)
+        if (ai >= a.t[q].offa) p = q;
+      const AddTerm& U = a.t[p];
+      out[e] = U.x[(ai - U.offa) + U.rl * (i0 + ii)];
+    }
+    return;
+  }
+  // interior: block diagonal
+  const double* x = T.x + T.rl * (i0 + a.I * (c - T.offc));
+  for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
+    const int64_t ai = e % RL, ii = e / RL;
+    const int64_t al = ai - T.offa;
+    out[e] = (al >= 0 && al < T.rl) ? x[al + T.rl * ii] : 0.0;
+  }
+}
+
+void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, int64_t I, int64_t RR, double* out) {
+  TTB_CHECK(nterms >= 1 && nterms <= kMaxAddTerms, TTB_ERR_CAPABILITY, "add: 1..16 terms supported");
+  if (I == 0 || RL == 0 || RR == 0) return;
+  AddArgs a;
+  a.mode = mode;
+  a.nterms = nterms;
+  for (int p = 0; p < nterms; ++p) a.t[p] = terms[p];
+  a.RL = RL;
+  a.I = I;
+  a.RR = RR;
+  a.ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
+  a.out = out;
+  TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "add: output right rank too large");
+  dim3 grid((unsigned)((I + a.ni - 1) / a.ni), (unsigned)RR);
+  add_kernel<<<grid, kEwNT, 0, ctx.stream>>>(a);
+  TTB_LAUNCHED();
+}
+
+// Z(a*rbl + c, i, b*rbr + d) = X(a, i, b) * Y(c, i, d)
+__global__ void __launch_bounds__(kEwNT)
+hadamard_kernel(const double* __restrict__ x, int64_t ral, int64_t rar, const double* __restrict__ y, int64_t rbl,
+                int64_t rbr, int64_t I, int ni, double* __restrict__ out) {
+  const int64_t col = blockIdx.y;
+  const int64_t bx = col / rbr, dy = col - bx * rbr;
+  const int64_t RL = ral * rbl;
+  const int64_t i0 = (int64_t)blockIdx.x * ni;
+  const int64_t nn = min64(ni, I - i0);
+  const int64_t cnt = RL * nn;
+  double* o = out + RL * (i0 + I * col);
+  const double* xs = x + ral * (i0 + I * bx);
+  const double* ys = y + rbl * (i0 + I * dy);
+  for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
+    const int64_t row = e % RL, ii = e / RL;
+    const int64_t ax = row / rbl, cy = row - ax * rbl;
+    o[e] = __dmul_rn(xs[ax + ral * ii], ys[cy + rbl * ii]);
+  }
+}
+
+void hadamard_core(Ctx& ctx, const double* x, int64_t ral, int64_t rar, const double* y, int64_t rbl, int64_t rbr,
+                   int64_t I, double* out) {
+  const int64_t RL = ral * rbl, RR = rar * rbr;
+  if (I == 0) return;
+  TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "hadamard: output right rank too large");
+  int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
+  dim3 grid((unsigned)((I + ni - 1) / ni), (unsigned)RR);
+  hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, out);
+  TTB_LAUNCHED();
+}
+
+__global__ void scale_kernel(int64_t n, const double* __restrict__ x, double s, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = __dmul_rn(s, x[e]);
+}
+
+void scale_vec(Ctx& ctx, int64_t n, const double* x, double s, double* out) {
+  if (n == 0) return;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 8);
+  scale_kernel<<<blocks, 256, 0, ctx.stream>>>(n, x, s, out);
+  TTB_LAUNCHED();
+}
+
+__global__ void fill_zero_kernel(double* p, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = 0.0;
+}
+
+void fill_zero(Ctx& ctx, double* p, int64_t n) {
+  if (n == 0) return;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 8);
+  fill_zero_kernel<<<blocks, 256, 0, ctx.stream>>>(p, n);
+  TTB_LAUNCHED();
+}
+
+// two-pass deterministic reduction: fixed grid, fixed per-thread order,
+// fixed-shape block trees, then one block sums the partials in order.
+constexpr int kRedBlocks = 512;
+
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(int64_t n, const double* __restrict__ x,
+                                                            double* __restrict__ part) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * 256LL + threadIdx.x; e < n; e += 256LL * kRedBlocks) acc = fma(x[e], x[e], acc);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) sum_final_kernel(int n, const double* __restrict__ part, double* res) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < n; e += 256) acc += part[e];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *res = red[0];
+}
+
+void sumsq_dev(Ctx& ctx, int64_t n, const double* x, double* dres) {
+  double* part = (double*)ctx.alloc(kRedBlocks * sizeof(double));
+  sumsq_partial_kernel<<<kRedBlocks, 256, 0, ctx.stream>>>(n, x, part);
+  TTB_LAUNCHED();
+  sum_final_kernel<<<1, 256, 0, ctx.stream>>>(kRedBlocks, part, dres);
+  TTB_LAUNCHED();
+  ctx.free(part);
+}
+
+}  // namespace ttb

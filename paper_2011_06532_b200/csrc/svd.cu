@@ -1,0 +1,207 @@
+// On-device truncated SVD of a small matrix (one-sided Hestenes-Jacobi),
+// replacing scipy gesdd + the tail rule of truncated_svd (parallel.py:224-258).
+//
+// One CTA.  A (m x n, m >= n, n <= 64; or its transpose) and V (n x n) live in
+// shared memory.  A round-robin tournament pairs all columns each round;
+// a group of 8 threads owns one pair: three dot products (reduced with
+// shuffles over the 8 lanes), one Rutishauser rotation, column updates.
+// Sweeps repeat until no pair exceeds the orthogonality threshold.
+// Afterwards sigma_j = ||a_j||, columns are ranked by sigma (descending,
+// ties by index, deterministic), and the reference's tail rule picks keep.
+//
+// Outputs (all device):
+//   C (m x keep, ld m)  = sorted columns of A V        (= U_k diag(s_k))
+//   Vk (n x keep, ld n) = sorted columns of V          (right vectors)
+//   s (n)               = sorted singular values (all n)
+//   info[0] = keep, info[1] = capped ; dinfo[0] = discarded tail
+#include "ctx.cuh"
+#include "svd.cuh"
+
+namespace ttb {
+
+constexpr int kSvdNT = 256;
+constexpr int kSvdMax = 64;
+constexpr int kGrp = 8;  // threads per column pair
+
+struct SvdSmem {
+  double A[kSvdMax * kSvdMax];   // ld = kSvdMax
+  double V[kSvdMax * kSvdMax];
+  double sig[kSvdMax];
+  int order[kSvdMax];
+  int slot[kSvdMax];             // tournament position -> column
+  int rotated;
+  int bad;
+};
+
+// reduction over the 8 lanes of one pair group; the mask names only those
+// lanes because neighbouring groups of the warp may be idle (padding pair)
+__device__ __forceinline__ double grp_sum(double v) {
+  const unsigned mask = 0xFFu << ((threadIdx.x & 31) & ~(kGrp - 1));
+#pragma unroll
+  for (int off = kGrp / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
+  return v;
+}
+
+__global__ void __launch_bounds__(kSvdNT, 1)
+jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int transA, double eps,
+                  int max_rank, double* __restrict__ C, double* __restrict__ Vk, double* __restrict__ s_out,
+                  int* __restrict__ info, double* __restrict__ dinfo) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SvdSmem& sm = *reinterpret_cast<SvdSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int np = (n + 1) & ~1;  // even number of tournament slots (pad column is zero)
+  if (tid == 0) sm.bad = 0;
+  __syncthreads();
+  for (int idx = tid; idx < kSvdMax * np; idx += kSvdNT) {
+    const int r = idx % kSvdMax, c = idx / kSvdMax;
+    double v = 0.0;
+    if (r < m && c < n) v = transA ? Ain[c + (int64_t)lda * r] : Ain[r + (int64_t)lda * c];
+    if (!isfinite(v)) { sm.bad = 1; v = 0.0; }
+    sm.A[r + kSvdMax * c] = v;
+    sm.V[r + kSvdMax * c] = (r == c && c < n) ? 1.0 : 0.0;
+  }
+  for (int c = tid; c < np; c += kSvdNT) sm.slot[c] = c;
+  __syncthreads();
+
+  const int grp = tid / kGrp, gl = tid % kGrp;
+  const int npairs = np / 2;
+  const double tol = 4.0 * 2.220446049250313e-16 * sqrt((double)m);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) sm.rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < np - 1; ++round) {
+      // pair grp: slots (grp, np-1-grp) of the current tournament table
+      for (int pr = grp; pr < npairs; pr += kSvdNT / kGrp) {
+        int p = sm.slot[pr], q = sm.slot[np - 1 - pr];
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q < n) {
+          double* ap = sm.A + kSvdMax * p;
+          double* aq = sm.A + kSvdMax * q;
+          double al = 0.0, be = 0.0, ga = 0.0;
+          for (int r = gl; r < m; r += kGrp) {
+            const double x = ap[r], y = aq[r];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+          al = grp_sum(al);
+          be = grp_sum(be);
+          ga = grp_sum(ga);
+          if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+            for (int r = gl; r < m; r += kGrp) {
+              const double x = ap[r], y = aq[r];
+              ap[r] = cs * x - sn * y;
+              aq[r] = sn * x + cs * y;
+            }
+            double* vp = sm.V + kSvdMax * p;
+            double* vq = sm.V + kSvdMax * q;
+            for (int r = gl; r < n; r += kGrp) {
+              const double x = vp[r], y = vq[r];
+              vp[r] = cs * x - sn * y;
+              vq[r] = sn * x + cs * y;
+            }
+            if (gl == 0) sm.rotated = 1;
+          }
+        }
+      }
+      __syncthreads();
+      // rotate the tournament table (slot 0 fixed)
+      if (tid == 0) {
+        const int last = sm.slot[np - 1];
+        for (int c = np - 1; c > 1; --c) sm.slot[c] = sm.slot[c - 1];
+        sm.slot[1] = last;
+      }
+      __syncthreads();
+    }
+    const int any = sm.rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  // singular values
+  for (int c = tid / 32; c < n; c += kSvdNT / 32) {
+    double acc = 0.0;
+    for (int r = tid % 32; r < m; r += 32) acc = fma(sm.A[r + kSvdMax * c], sm.A[r + kSvdMax * c], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((tid % 32) == 0) sm.sig[c] = sqrt(acc);
+  }
+  __syncthreads();
+  // deterministic ranking: position = #(larger) + #(equal with lower index)
+  for (int c = tid; c < n; c += kSvdNT) {
+    const double v = sm.sig[c];
+    int pos = 0;
+    for (int o = 0; o < n; ++o) {
+      const double w = sm.sig[o];
+      pos += (w > v) || (w == v && o < c);
+    }
+    sm.order[pos] = c;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // tail_sq[k] = sum_{j >= k} s_j^2, accumulated from the smallest up
+    double tail = 0.0;
+    int keep = n;  // tail_sq[n] = 0 <= eps^2 always
+    double tails[kSvdMax + 1];
+    tails[n] = 0.0;
+    for (int k = n - 1; k >= 0; --k) {
+      const double sv = sm.sig[sm.order[k]];
+      tail += sv * sv;
+      tails[k] = tail;
+    }
+    const double e2 = eps * eps;
+    for (int k = 0; k <= n; ++k) {
+      if (tails[k] <= e2) { keep = k; break; }
+    }
+    if (keep < 1) keep = 1;
+    int capped = 0;
+    if (max_rank > 0 && keep > max_rank) { keep = max_rank; capped = 1; }
+    info[0] = keep;
+    info[1] = capped;
+    info[2] = sm.bad;
+    dinfo[0] = sqrt(tails[keep]);
+  }
+  for (int k = tid; k < n; k += kSvdNT) s_out[k] = sm.sig[sm.order[k]];
+  __syncthreads();
+  const int keep = info[0];
+  for (int idx = tid; idx < m * keep; idx += kSvdNT) {
+    const int r = idx % m, k = idx / m;
+    C[r + (int64_t)m * k] = sm.A[r + kSvdMax * sm.order[k]];
+  }
+  for (int idx = tid; idx < n * keep; idx += kSvdNT) {
+    const int r = idx % n, k = idx / n;
+    Vk[r + (int64_t)n * k] = sm.V[r + kSvdMax * sm.order[k]];
+  }
+}
+
+// normalize C columns into U (sigma == 0 -> unit vector e_k)
+__global__ void svd_u_kernel(const double* C, const double* s, int m, int keep, double* U) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < m * keep; idx += blockDim.x * gridDim.x) {
+    const int r = idx % m, k = idx / m;
+    const double sv = s[k];
+    U[idx] = sv > 0.0 ? C[idx] / sv : (r == k ? 1.0 : 0.0);
+  }
+}
+
+void jacobi_svd(Ctx& ctx, const double* A, int lda, int m, int n, bool transA, double eps, int max_rank,
+                double* C, double* Vk, double* s, int* info, double* dinfo) {
+  TTB_CHECK(m >= n && n >= 1 && m <= kSvdMax, TTB_ERR_CAPABILITY, "Jacobi SVD: need 1 <= n <= m <= 64");
+  static bool attr = false;
+  if (!attr) {
+    TTB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SvdSmem)));
+    attr = true;
+  }
+  jacobi_svd_kernel<<<1, kSvdNT, sizeof(SvdSmem), ctx.stream>>>(A, lda, m, n, transA ? 1 : 0, eps, max_rank, C, Vk,
+                                                               s, info, dinfo);
+  TTB_LAUNCHED();
+}
+
+void svd_normalize_u(Ctx& ctx, const double* C, const double* s, int m, int keep, double* U) {
+  svd_u_kernel<<<1, 256, 0, ctx.stream>>>(C, s, m, keep, U);
+  TTB_LAUNCHED();
+}
+
+}  // namespace ttb

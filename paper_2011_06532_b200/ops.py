@@ -1,0 +1,179 @@
+"""TT arithmetic on device-resident tensors (drop-in for ttpar.ops).
+
+scale / add / hadamard are slab-local (no communication, ops.py:1-8);
+inner_product / norm are Gram sweeps with one r x r allreduce per mode
+(ops.py:135-235).  Host TTTensor arguments are uploaded to the current GPU,
+processed there, and returned as host TTTensor (the sequential flavour of
+the reference API); DistTTTensor stays on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from math import sqrt
+
+from . import _lib
+from .comm import default_comm
+from .errors import CapacityError, ContractError, ShapeError
+from .tensor import DistTTTensor, TTTensor, f_empty, to_host_array
+
+NORM_METHODS = ("innerprod", "innerprod_sym", "ortho")
+HADAMARD_RANK_GUARD = 4096  # ops.py:38
+
+
+def _as_dist(x):
+    """(DistTTTensor, is_host) for either flavour (ops.py:44-50)."""
+    if isinstance(x, DistTTTensor):
+        return x, False
+    if isinstance(x, TTTensor):
+        comm = default_comm()
+        return DistTTTensor(comm, x.dims, x.ranks, [c.array for c in x.cores]), True
+    raise ContractError(f"expected TTTensor or DistTTTensor, got {type(x).__name__}")
+
+
+def _to_host(dt):
+    return TTTensor([to_host_array(s) for s in dt.local])
+
+
+def _check_pair(x, y):
+    if isinstance(x, DistTTTensor) != isinstance(y, DistTTTensor):
+        if isinstance(x, (TTTensor, DistTTTensor)) and isinstance(y, (TTTensor, DistTTTensor)):
+            raise ContractError("cannot mix sequential and distributed tensors")
+    dx, hx = _as_dist(x)
+    dy, hy = _as_dist(y)
+    if not hx and dx.comm is not dy.comm:
+        raise ContractError("operands live on different communicators")
+    if dx.dims != dy.dims:
+        raise ShapeError(f"dimension mismatch: {dx.dims} vs {dy.dims}")
+    if hx:
+        dy = DistTTTensor(dx.comm, dy.dims, dy.ranks, dy.local)
+    return dx, dy, hx
+
+
+def _ptrs(slabs):
+    return _lib.ptr_array([s.data_ptr() for s in slabs])
+
+
+def scale(x, s: float):
+    """Scalar multiple folded into core 0 (ops.py:71-76)."""
+    dt, host = _as_dist(x)
+    lib = _lib.load()
+    ctx = dt.comm.ctx()
+    out = []
+    for n, sl in enumerate(dt.local):
+        o = f_empty(*sl.shape, dt.comm.device)
+        if n == 0:
+            _lib.check(lib.ttb_scale(ctx, sl.numel(), C.c_void_p(sl.data_ptr()), float(s), C.c_void_p(o.data_ptr())))
+        else:
+            o.copy_(sl)
+        out.append(o)
+    res = DistTTTensor(dt.comm, dt.dims, dt.ranks, out)
+    return _to_host(res) if host else res
+
+
+def add_n(terms, scales=None):
+    """Fused N-ary sum  sum_p scales[p] * terms[p]  in one pass per core.
+
+    Equivalent to nesting add(scale(a, s0), scale(b, s1)) ... (ops.py:71-106)
+    bit for bit: blocks are placed in term order and the scales multiply
+    core 0 only; each output element is written once.
+    """
+    if not terms:
+        raise ContractError("add_n needs at least one term")
+    dts = []
+    host = None
+    for t in terms:
+        d, h = _as_dist(t)
+        if host is None:
+            host = h
+        elif host != h:
+            raise ContractError("cannot mix sequential and distributed tensors")
+        dts.append(d)
+    base = dts[0]
+    if host:
+        dts = [base] + [DistTTTensor(base.comm, d.dims, d.ranks, d.local) for d in dts[1:]]
+    for d in dts[1:]:
+        if d.dims != base.dims:
+            raise ShapeError(f"dimension mismatch: {base.dims} vs {d.dims}")
+        if d.comm is not base.comm:
+            raise ContractError("operands live on different communicators")
+    N = base.ndim
+    scales = [1.0] * len(dts) if scales is None else [float(s) for s in scales]
+    if N == 1:
+        out_ranks = (1, 1)
+    else:
+        mid = [sum(d.ranks[n] for d in dts) for n in range(1, N)]
+        out_ranks = (1,) + tuple(mid) + (1,)
+    ldims = base.local_dims()
+    outs = [f_empty(out_ranks[n], ldims[n], out_ranks[n + 1], base.comm.device) for n in range(N)]
+    lib = _lib.load()
+    ranks_flat = [r for d in dts for r in d.ranks]
+    cores_flat = [s.data_ptr() for d in dts for s in d.local]
+    _lib.check(lib.ttb_add(base.comm.ctx(), len(dts), N, _lib.i64_array(ldims), _lib.i64_array(ranks_flat),
+                           _lib.ptr_array(cores_flat), (C.c_double * len(scales))(*scales), _ptrs(outs)))
+    res = DistTTTensor(base.comm, base.dims, out_ranks, outs)
+    return _to_host(res) if host else res
+
+
+def add(x, y):
+    """TT sum: end cores concatenate, interior cores stack block-diagonally
+    (ops.py:79-106).  Bond ranks add; no data moves between ranks."""
+    dx, dy, host = _check_pair(x, y)
+    res = add_n([dx, dy])
+    return _to_host(res) if host else res
+
+
+def hadamard(x, y, max_rank_product: int | None = None):
+    """Elementwise product: slice-wise Kronecker cores (ops.py:109-132)."""
+    dx, dy, host = _check_pair(x, y)
+    guard = HADAMARD_RANK_GUARD if max_rank_product is None else int(max_rank_product)
+    ranks = tuple(a * b for a, b in zip(dx.ranks, dy.ranks))
+    if max(ranks) > guard:
+        raise CapacityError(f"hadamard bond ranks {max(ranks)} exceed the guard ({guard}); "
+                            "round the operands first or raise max_rank_product")
+    ldims = dx.local_dims()
+    outs = [f_empty(ranks[n], ldims[n], ranks[n + 1], dx.comm.device) for n in range(dx.ndim)]
+    lib = _lib.load()
+    _lib.check(lib.ttb_hadamard(dx.comm.ctx(), dx.ndim, _lib.i64_array(ldims), _lib.i64_array(dx.ranks),
+                                _lib.i64_array(dy.ranks), _ptrs(dx.local), _ptrs(dy.local), _ptrs(outs)))
+    res = DistTTTensor(dx.comm, dx.dims, ranks, outs)
+    return _to_host(res) if host else res
+
+
+def inner_product(x, y) -> float:
+    """<x, y> by the Gram recurrence, one allreduce per mode (ops.py:135-155)."""
+    dx, dy, _ = _check_pair(x, y)
+    lib = _lib.load()
+    res = C.c_double(0.0)
+    _lib.check(lib.ttb_inner(dx.comm.ctx(), dx.ndim, _lib.i64_array(dx.local_dims()), _lib.i64_array(dx.ranks),
+                             _lib.i64_array(dy.ranks), _ptrs(dx.local), _ptrs(dy.local), C.byref(res)))
+    return float(res.value)
+
+
+def _sumsq(comm, slab):
+    lib = _lib.load()
+    res = C.c_double(0.0)
+    _lib.check(lib.ttb_sumsq(comm.ctx(), slab.numel(), C.c_void_p(slab.data_ptr()), C.byref(res)))
+    return float(res.value)
+
+
+def norm(x, method: str = "innerprod", return_info: bool = False):
+    """Frobenius norm by one of three routes (ops.py:208-235).
+
+    ``innerprod``: sqrt(<x, x>) with the fused Gram kernel.
+    ``innerprod_sym``: the same Gram sweep (the device kernel already fuses
+    both products; it never falls back).  ``ortho``: right-orthonormalize a
+    copy and read the norm off core 0 (no cancellation floor).
+    """
+    if method not in NORM_METHODS:
+        raise ContractError(f"unknown norm method {method!r}; pick from {NORM_METHODS}")
+    info = {"method": method, "fallback": False}
+    dx, _ = _as_dist(x)
+    if method in ("innerprod", "innerprod_sym"):
+        val = sqrt(max(inner_product(dx, dx), 0.0))
+    else:
+        from .parallel import orthonormalize
+
+        o = orthonormalize(dx, "right")
+        val = sqrt(max(_sumsq(dx.comm, o.local[0]), 0.0))
+    return (val, info) if return_info else val
