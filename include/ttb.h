@@ -133,6 +133,11 @@ int ttb_truncated_svd(ttb_ctx* ctx, int64_t m, int64_t n, const double* a, doubl
                       int64_t max_rank, double* u, double* s, double* v, int64_t* keep,
                       double* tail, int* capped);
 
+/* opt-in per-kernel-class timing with CUDA events (benchmark roofline);
+ * dump writes "name launches total_ms\n" lines and clears the record. */
+int ttb_prof_enable(int on);
+int ttb_prof_dump(char* buf, long long cap);
+
 /* measured fp64 throughput of this device (TFLOP/s): scalar DFMA and
  * warp-level DMMA (mma.sync m8n8k4 f64).  Roofline denominators. */
 int ttb_fp64_peak(void* stream, double* dfma_tflops, double* dmma_tflops);

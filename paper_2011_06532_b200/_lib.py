@@ -56,6 +56,8 @@ SIGNATURES = {
     "ttb_truncated_svd": (C.c_int, [_P, _I64, _I64, _P, C.c_double, _I64, _P, _P, _P, _PI64, _PD,
                                     C.POINTER(C.c_int)]),
     "ttb_fp64_peak": (C.c_int, [_P, _PD, _PD]),
+    "ttb_prof_enable": (C.c_int, [C.c_int]),
+    "ttb_prof_dump": (C.c_int, [C.c_char_p, C.c_longlong]),
 }
 
 _lib = None
@@ -99,3 +101,24 @@ def ptr_array(ptrs):
 
 def launch_counter():
     return int(load().ttb_launch_counter())
+
+
+def prof_enable(on=True):
+    check(load().ttb_prof_enable(1 if on else 0))
+
+
+def prof_dump():
+    """{kernel class: (launches, total_ms)} recorded since the last dump."""
+    buf = C.create_string_buffer(1 << 16)
+    check(load().ttb_prof_dump(buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out
+
+
+def fp64_peak(stream=0):
+    a, b = C.c_double(), C.c_double()
+    check(load().ttb_fp64_peak(C.c_void_p(stream), C.byref(a), C.byref(b)))
+    return float(a.value), float(b.value)

@@ -41,6 +41,7 @@ def build(force=False, verbose=False, jobs=None):
              "--expt-relaxed-constexpr"] + ARCH
     if verbose:
         flags += ["-Xptxas", "-v"]
+    flags += os.environ.get("NVCC_EXTRA", "").split()
     objs = []
     procs = []
     for src in sources():

@@ -120,6 +120,13 @@ int ttb_ctx_create(int device, void* stream, ttb_ctx** out) {
     TTB_THROW(TTB_ERR_CAPABILITY, "this build targets sm_100a (B200); device is sm_" +
                                       std::to_string(cc_major) + std::to_string(cc_minor));
   }
+  // keep freed workspace mapped in the stream-ordered pool: the default
+  // release threshold (0) unmaps it at every stream sync, which costs more
+  // than the kernels (GB-sized TSQR factors are re-allocated every call)
+  cudaMemPool_t pool;
+  TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  TTB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   *out = c;
   TTB_TRY_END
 }

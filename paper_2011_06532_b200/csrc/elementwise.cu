@@ -9,6 +9,7 @@
 // IEEE sequence of the reference (one multiply, left-to-right sums, no FMA
 // contraction) so results are bitwise identical to numpy.
 #include "ops.cuh"
+#include "prof.cuh"
 
 namespace ttb {
 
@@ -85,6 +86,7 @@ void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, 
   a.out = out;
   TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "add: output right rank too large");
   dim3 grid((unsigned)((I + a.ni - 1) / a.ni), (unsigned)RR);
+  ProfScope ps("add", ctx.stream);
   add_kernel<<<grid, kEwNT, 0, ctx.stream>>>(a);
   TTB_LAUNCHED();
 }
@@ -116,6 +118,7 @@ void hadamard_core(Ctx& ctx, const double* x, int64_t ral, int64_t rar, const do
   TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "hadamard: output right rank too large");
   int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
   dim3 grid((unsigned)((I + ni - 1) / ni), (unsigned)RR);
+  ProfScope ps("hadamard", ctx.stream);
   hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, out);
   TTB_LAUNCHED();
 }
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(256) sum_final_kernel(int n, const double* __r
 
 void sumsq_dev(Ctx& ctx, int64_t n, const double* x, double* dres) {
   double* part = (double*)ctx.alloc(kRedBlocks * sizeof(double));
+  ProfScope ps("sumsq", ctx.stream);
   sumsq_partial_kernel<<<kRedBlocks, 256, 0, ctx.stream>>>(n, x, part);
   TTB_LAUNCHED();
   sum_final_kernel<<<1, 256, 0, ctx.stream>>>(kRedBlocks, part, dres);

@@ -8,6 +8,7 @@
 // The small matrix sits in shared memory; the big operand streams through
 // once, coalesced, and every output element is written once.
 #include "ops.cuh"
+#include "prof.cuh"
 
 namespace ttb {
 
@@ -65,6 +66,7 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
   const size_t smem = (size_t)(M * K + K * kGlNB) * sizeof(double);
   TTB_CUDA(cudaFuncSetAttribute(gemm_small_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t blocks = std::min<int64_t>((N + kGlNB - 1) / kGlNB, (int64_t)ctx.num_sms * 4);
+  ProfScope ps("fold_left", ctx.stream);
   gemm_small_left_kernel<<<(int)blocks, kGlNT, smem, ctx.stream>>>(M, K, N, F, ldf, transF ? 1 : 0, H, out);
   TTB_LAUNCHED();
 }
@@ -99,6 +101,7 @@ void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, cons
   TTB_CHECK(K <= 64 && Nn <= 64, TTB_ERR_CAPABILITY, "fold: small dimension above 64");
   if (Mb == 0 || Nn == 0) return;
   const int blocks = (int)std::min<int64_t>((Mb + 255) / 256, (int64_t)ctx.num_sms * 8);
+  ProfScope ps("fold_right", ctx.stream);
   if (Nn <= 16)
     gemm_small_right_kernel<16><<<blocks, 256, 0, ctx.stream>>>(Mb, K, Nn, V, G, ldg, transG ? 1 : 0, out);
   else if (Nn <= 32)

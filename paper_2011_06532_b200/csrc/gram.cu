@@ -8,6 +8,7 @@
 // and writes one partial W; a second kernel sums the CTA partials in a
 // fixed order (bitwise deterministic, no atomics).
 #include "ops.cuh"
+#include "prof.cuh"
 
 namespace ttb {
 
@@ -165,6 +166,7 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
   double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
   GramArgs a{W, X, Y, (int)ral, (int)rar, (int)rbl, (int)rbr, I, ns, per_cta, part};
   TTB_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfScope ps("gram", ctx.stream);
   gram_kernel<<<grid, kGrNT, smem, ctx.stream>>>(a);
   TTB_LAUNCHED();
   gram_final_kernel<<<(int)std::max<int64_t>(1, (cnt + 255) / 256), 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);

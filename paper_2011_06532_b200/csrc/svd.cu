@@ -15,6 +15,7 @@
 //   s (n)               = sorted singular values (all n)
 //   info[0] = keep, info[1] = capped ; dinfo[0] = discarded tail
 #include "ctx.cuh"
+#include "prof.cuh"
 #include "svd.cuh"
 
 namespace ttb {
@@ -72,7 +73,10 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     for (int round = 0; round < np - 1; ++round) {
       // pair grp: slots (grp, np-1-grp) of the current tournament table
       for (int pr = grp; pr < npairs; pr += kSvdNT / kGrp) {
-        int p = sm.slot[pr], q = sm.slot[np - 1 - pr];
+        // circle-method round robin: player np-1 fixed, the rest rotate
+        const int M1 = np - 1;
+        int p = pr == 0 ? M1 : (round + pr) % M1;
+        int q = pr == 0 ? round : (round - pr + M1) % M1;
         if (p > q) { int t = p; p = q; q = t; }
         if (q < n) {
           double* ap = sm.A + kSvdMax * p;
@@ -107,13 +111,6 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
             if (gl == 0) sm.rotated = 1;
           }
         }
-      }
-      __syncthreads();
-      // rotate the tournament table (slot 0 fixed)
-      if (tid == 0) {
-        const int last = sm.slot[np - 1];
-        for (int c = np - 1; c > 1; --c) sm.slot[c] = sm.slot[c - 1];
-        sm.slot[1] = last;
       }
       __syncthreads();
     }
@@ -194,6 +191,7 @@ void jacobi_svd(Ctx& ctx, const double* A, int lda, int m, int n, bool transA, d
     TTB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SvdSmem)));
     attr = true;
   }
+  ProfScope ps("jacobi_svd", ctx.stream);
   jacobi_svd_kernel<<<1, kSvdNT, sizeof(SvdSmem), ctx.stream>>>(A, lda, m, n, transA ? 1 : 0, eps, max_rank, C, Vk,
                                                                s, info, dinfo);
   TTB_LAUNCHED();

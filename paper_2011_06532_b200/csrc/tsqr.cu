@@ -1,7 +1,10 @@
 // TSQR kernels (leaf chain, tree nodes, apply) and the host-side factor object.
 // See tsqr.cuh for the decomposition.  Reference: ttpar tsqr.py:103-327.
+#include <vector>
+
 #include "tsqr.cuh"
 #include "ctx.cuh"
+#include "prof.cuh"
 
 namespace ttb {
 
@@ -23,6 +26,7 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
   const int64_t tb = plan.tile_base(g);
 
   double A[C::RPL][C::CPL];
+  init_ring<C>(sm);
   for (int t = 0; t < ntiles; ++t) {
     const int64_t ia = s0 + (int64_t)t * ni;
     const int nsl = (int)min64(ni, n_g - (int64_t)t * ni);
@@ -30,7 +34,7 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     // load (zero padded)
 #pragma unroll
     for (int s = 0; s < C::RPL; ++s) {
-      const int r = s * C::LR + lr;
+      const int r = C::row(s, lr);
       int si, w;
       tile_row(P.trans, r, nsl, rs, si, w);
 #pragma unroll
@@ -42,10 +46,10 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     zero_G<C>(sm);
     __syncthreads();
     const bool head = (t == 0);
-    tile_qr<C>(A, b, head, sm);
+    tile_qr<C>(A, b, head, sm, t * b);
     const int64_t tile = tb + t;
     store_Y<C>(A, b, head, Yg + tile * (int64_t)C::MC * b, C::MC);
-    store_T<C>(sm, b, Tg + tile * (int64_t)b * b);
+    store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
     if (head) extract_R<C>(A, b, sm);
     __syncthreads();
   }
@@ -71,7 +75,7 @@ tsqr_tree_kernel(const double* __restrict__ Rin, int n_in, int b, int f, double*
   double A[C::RPL][C::CPL];
 #pragma unroll
   for (int s = 0; s < C::RPL; ++s) {
-    const int r = s * C::LR + lr;
+    const int r = C::row(s, lr);
     const int ch = r / b, rr = r - ch * b;
 #pragma unroll
     for (int u = 0; u < C::CPL; ++u) {
@@ -80,10 +84,11 @@ tsqr_tree_kernel(const double* __restrict__ Rin, int n_in, int b, int f, double*
     }
   }
   zero_G<C>(sm);
+  init_ring<C>(sm);
   __syncthreads();
-  tile_qr<C>(A, b, true, sm);
+  tile_qr<C>(A, b, true, sm, 0);
   store_Y<C>(A, b, true, Yn + (int64_t)q * C::MC * b, C::MC);
-  store_T<C>(sm, b, Tn + (int64_t)q * b * b);
+  store_T<C>(sm, b, Tn + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
   extract_R<C>(A, b, sm);
   __syncthreads();
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
@@ -104,152 +109,255 @@ __global__ void sign_fix_kernel(const double* __restrict__ R, int b, double* __r
 }
 
 // ------------------------------------------------------------------------
-// apply kernel: out(rows of this CTA) = Q [D z0; 0]
+// apply: out = Q [D z0; 0], in three launches
+//   1. tree levels, top-down: one CTA per node computes every child's
+//      b x k block  z_c = [z;0]_c - V_c T V_top^T z   (written once, not
+//      recomputed by every leaf CTA)
+//   2. chains: one CTA per leaf chain walks its tiles in reverse with the
+//      compact-WY T factors only: u_t = T_t z_t (head: T_0 V_top^T z_0),
+//      z_{t-1} = z_t - u_t; writes every u_t (and z_0) to scratch
+//   3. products: one CTA per tile, fully parallel: out_t = -Y_t u_t
+//      (+ z_0 on the head tile's top rows); Y_t streamed into shared memory
+//      by the bulk-copy (TMA) engine, 4x4 register blocks
 // ------------------------------------------------------------------------
 constexpr int kApplyNT = 256;
-constexpr int kApplyBM = 64;   // max b
 constexpr int kApplyKM = 64;   // max k
-constexpr int kApplyCW = 16;   // output columns per thread pass
 
-struct ApplyArgs {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// one thread: copy `bytes` (multiple of 16) from global to shared, signalling bar
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  mbar_expect_tx(bar, bytes);
+  constexpr unsigned kChunk = 32768;
+  for (unsigned off = 0; off < bytes; off += kChunk) {
+    const unsigned n = bytes - off < kChunk ? bytes - off : kChunk;
+    bulk_g2s((char*)dst + off, (const char*)src + off, n, bar);
+  }
+}
+
+__host__ __device__ __forceinline__ int64_t tstride_of(int b) { return ((int64_t)b * b + 1) & ~1LL; }
+__host__ __device__ __forceinline__ int kpad(int k) { return (k + 3) & ~3; }
+
+// Out[i + b*c] = sum_{l >= i} M(i, l) In[l + b*c]; M(i,l) = vtop ? M[l + ldm*i] : M[i + ldm*l]
+__device__ __forceinline__ void tri_gemm(const double* M, int ldm, bool vtop, const double* In, double* Out, int b,
+                                         int k) {
+  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+    const int i = idx % b, c = idx / b;
+    double a0 = 0.0, a1 = 0.0;
+    int l = i;
+    for (; l + 1 < b; l += 2) {
+      const double m0 = vtop ? M[l + ldm * i] : M[i + ldm * l];
+      const double m1 = vtop ? M[l + 1 + ldm * i] : M[i + ldm * (l + 1)];
+      a0 = fma(m0, In[l + b * c], a0);
+      a1 = fma(m1, In[l + 1 + b * c], a1);
+    }
+    if (l < b) a0 = fma(vtop ? M[l + ldm * i] : M[i + ldm * l], In[l + b * c], a0);
+    Out[idx] = a0 + a1;
+  }
+}
+
+// ---- 1. tree levels -------------------------------------------------------
+// zin: (nodes) blocks of b x k (ld b); zout: (nodes * f) child blocks.
+// D (optional) multiplies the rows of the root input (sign fix).
+__global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int nnodes_below, int b, int k,
+                                                                   const double* __restrict__ zin,
+                                                                   const double* __restrict__ D,
+                                                                   double* __restrict__ zout) {
+  extern __shared__ __align__(16) double tsm[];
+  const int q = blockIdx.x;
+  double* Z = tsm;            // b x k
+  double* W = Z + b * k;      // b x k
+  double* U = W + b * k;      // b x k
+  double* Vt = U + b * k;     // b x b (node rows 0..b-1)
+  double* Tm = Vt + b * b;    // b x b
+  const double* Yg = L.Y + (int64_t)q * L.ldy * b;
+  const double* Tg = L.T + (int64_t)q * tstride_of(b);
+  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+    const double d = D ? D[idx % b] : 1.0;
+    Z[idx] = d * zin[(int64_t)q * b * k + idx];
+  }
+  for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
+    Vt[idx] = Yg[idx % b + (int64_t)L.ldy * (idx / b)];
+    Tm[idx] = Tg[idx];
+  }
+  __syncthreads();
+  tri_gemm(Vt, b, true, Z, W, b, k);  // W = V_top^T Z
+  __syncthreads();
+  tri_gemm(Tm, b, false, W, U, b, k);  // U = T W
+  __syncthreads();
+  const int cnt = min(L.f, nnodes_below - q * L.f);
+  for (int idx = threadIdx.x; idx < cnt * b * k; idx += kApplyNT) {
+    const int c = idx / (b * k), rem = idx - c * b * k;
+    const int i = rem % b, cc = rem / b;
+    double acc = (c == 0) ? Z[i + b * cc] : 0.0;
+    const double* Vc = Yg + (int64_t)c * b + i;
+    for (int l = 0; l < b; ++l) acc = fma(-Vc[(int64_t)L.ldy * l], U[l + b * cc], acc);
+    zout[((int64_t)q * L.f + c) * b * k + rem] = acc;
+  }
+}
+
+// ---- 2. chains ------------------------------------------------------------
+struct ChainArgs {
   LeafPlan plan;
-  int ldy;                     // leaf tile rows (MC of the leaf config)
+  int ldy;
   const double* Y;
   const double* T;
-  TreeDesc local;              // levels above the CTA leaves, lev[0] lowest
-  TreeDesc global;             // levels above the rank roots (multi-GPU), lev[0] lowest
-  int rank;
-  const double* z0;            // b x k, col-major, ld b
+  const double* zin;     // per CTA b x k (ld b)
+  const double* D;       // sign fix when there is no tree above (else null)
   int k;
-  const double* D;             // b signs or nullptr
-  Panel out;                   // output view with k columns
+  double* u;             // per tile b x KP, row-major (l*KP + c)
+  double* z0;            // per CTA b x k: the head tile's input z_0
 };
 
-struct ApplySmem {
-  double Z[kApplyBM * kApplyKM];
-  double W[kApplyBM * kApplyKM];
-  double U[kApplyBM * kApplyKM];
-};
-
-// S_out[i, c] = sum_l M(i, l) * S_in[l, c],  M(i,l) = trans ? Mg[l + ld*i] : Mg[i + ld*l]
-// lo_tri != 0: M(i, l) vanishes for l < i (T upper, V_top^T upper)
-__device__ __forceinline__ void small_gemm(const double* __restrict__ Mg, int ld, bool trans, int lo_tri,
-                                           const double* Sin, double* Sout, int b, int k) {
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, c = idx / b;
-    double acc = 0.0;
-    const int l0 = lo_tri ? i : 0, l1 = b;  // triangular operands: l >= i
-    for (int l = l0; l < l1; ++l) {
-      const double m = trans ? Mg[l + (int64_t)ld * i] : Mg[i + (int64_t)ld * l];
-      acc = fma(m, Sin[l + kApplyBM * c], acc);
-    }
-    Sout[i + kApplyBM * c] = acc;
-  }
-}
-
-// One tree level: z <- rows of child c of Q_node [z; 0]
-__device__ void apply_node(ApplySmem& sm, const Level& L, int q, int c, int b, int k) {
-  const double* Y = L.Y + (int64_t)q * L.ldy * b;
-  const double* T = L.T + (int64_t)q * b * b;
-  // W = V_top^T Z   (V_top unit lower triangular: V_top^T upper)
-  small_gemm(Y, L.ldy, true, 2, sm.Z, sm.W, b, k);
-  __syncthreads();
-  small_gemm(T, b, false, 1, sm.W, sm.U, b, k);   // U = T W
-  __syncthreads();
-  // Z <- [Z;0]_child - V_child U
-  const double* Vc = Y + (int64_t)c * b;
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, cc = idx / b;
-    double acc = (c == 0) ? sm.Z[i + kApplyBM * cc] : 0.0;
-    for (int l = 0; l < b; ++l) acc = fma(-Vc[i + (int64_t)L.ldy * l], sm.U[l + kApplyBM * cc], acc);
-    sm.W[i + kApplyBM * cc] = acc;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, cc = idx / b;
-    sm.Z[i + kApplyBM * cc] = sm.W[i + kApplyBM * cc];
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kApplyNT, 2) tsqr_apply_kernel(ApplyArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ApplySmem& sm = *reinterpret_cast<ApplySmem*>(smem_raw);
+__global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int g = blockIdx.x;
   const LeafPlan& pl = a.plan;
-  const int b = pl.b, k = a.k, rs = pl.rs, ni = pl.ni, ldy = a.ldy;
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, c = idx / b;
-    const double d = a.D ? a.D[i] : 1.0;
-    sm.Z[i + kApplyBM * c] = d * a.z0[i + (int64_t)b * c];
-  }
-  __syncthreads();
-  // global levels (identical on every rank), top-down, leaf index = rank
-  for (int L = a.global.nlev - 1; L >= 0; --L) {
-    const Level& lv = a.global.lev[L];
-    int x = a.rank;
-    for (int u = 0; u < L; ++u) x /= lv.f;
-    apply_node(sm, lv, x / lv.f, x % lv.f, b, k);
-  }
-  // local levels, leaf index = CTA
-  for (int L = a.local.nlev - 1; L >= 0; --L) {
-    const Level& lv = a.local.lev[L];
-    int x = g;
-    for (int u = 0; u < L; ++u) x /= lv.f;
-    apply_node(sm, lv, x / lv.f, x % lv.f, b, k);
-  }
-  // chain, last tile first
-  const int64_t n_g = pl.count(g), s0 = pl.start(g);
+  const int b = pl.b, k = a.k, KP = kpad(k);
+  const int64_t tsz = tstride_of(b);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // T double buffer
+  double* Z = reinterpret_cast<double*>(smem_raw + 64);
+  double* U = Z + ((b * k + 1) & ~1);
+  double* W = U + ((b * k + 1) & ~1);
+  double* Tb0 = W + ((b * k + 1) & ~1);
+  double* Tb1 = Tb0 + tsz;
+  const int64_t n_g = pl.count(g);
   const int ntiles = pl.tiles_of(n_g);
   const int64_t tb = pl.tile_base(g);
-  for (int t = ntiles - 1; t >= 0; --t) {
-    const int64_t tile = tb + t;
-    const double* Y = a.Y + tile * (int64_t)ldy * b;
-    const double* T = a.T + tile * (int64_t)b * b;
-    const bool head = (t == 0);
-    if (head) {
-      small_gemm(Y, ldy, true, 2, sm.Z, sm.W, b, k);  // W = V_top^T Z
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+    const double d = a.D ? a.D[idx % b] : 1.0;
+    Z[idx] = d * a.zin[(int64_t)g * b * k + idx];
+  }
+  __syncthreads();
+  const unsigned tbytes = (unsigned)(tsz * 8);
+  if (threadIdx.x == 0) {
+    bulk_load(Tb0, a.T + (tb + ntiles - 1) * tsz, tbytes, &bars[0]);
+    if (ntiles > 1) bulk_load(Tb1, a.T + (tb + ntiles - 2) * tsz, tbytes, &bars[1]);
+  }
+  for (int t = ntiles - 1, it = 0; t >= 0; --t, ++it) {
+    const int cur = it & 1;
+    double* Tc = cur ? Tb1 : Tb0;
+    mbar_wait(&bars[cur], (it >> 1) & 1);
+    double* ut = a.u + (tb + t) * (int64_t)b * KP;
+    if (t == 0) {
+      // head: u_0 = T_0 (V_top^T z_0), V_top = rows 0..b-1 of Y_0 (global)
+      const double* Y0 = a.Y + tb * (int64_t)a.ldy * b;
+      tri_gemm(Y0, a.ldy, true, Z, W, b, k);
       __syncthreads();
-      small_gemm(T, b, false, 1, sm.W, sm.U, b, k);   // U = T W
+      tri_gemm(Tc, b, false, W, U, b, k);
+      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) a.z0[(int64_t)g * b * k + idx] = Z[idx];
     } else {
-      small_gemm(T, b, false, 1, sm.Z, sm.U, b, k);   // U = T Z
+      tri_gemm(Tc, b, false, Z, U, b, k);  // U = T_t Z
     }
     __syncthreads();
-    const int64_t ia = s0 + (int64_t)t * ni;
-    const int nsl = (int)min64(ni, n_g - (int64_t)t * ni);
-    const int rows = nsl * rs;
-    const int ncg = (k + kApplyCW - 1) / kApplyCW;
-    for (int idx = threadIdx.x; idx < ldy * ncg; idx += kApplyNT) {
-      const int r = idx % ldy, cg = idx / ldy;
+    for (int idx = threadIdx.x; idx < b * KP; idx += kApplyNT) {
+      const int l = idx / KP, c = idx % KP;
+      ut[idx] = c < k ? U[l + b * c] : 0.0;
+    }
+    if (t > 0)
+      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) Z[idx] -= U[idx];
+    __syncthreads();
+    if (threadIdx.x == 0 && t >= 2) {
+      fence_proxy_async();
+      bulk_load(Tc, a.T + (tb + t - 2) * tsz, tbytes, &bars[cur]);
+    }
+  }
+}
+
+// ---- 3. products ----------------------------------------------------------
+struct ProductArgs {
+  LeafPlan plan;
+  int ldy;
+  const double* Y;
+  const double* u;
+  const double* z0;
+  int k;
+  Panel out;
+};
+
+__global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const LeafPlan& pl = a.plan;
+  const int b = pl.b, k = a.k, KP = kpad(k), ldy = a.ldy, rs = pl.rs, ni = pl.ni;
+  const int64_t tile = blockIdx.x;
+  // tile -> (CTA g, position t) of the factor's chains
+  const int rem = pl.rem();
+  const int64_t t1 = pl.tiles_of(pl.base() + 1), t0 = pl.tiles_of(pl.base());
+  int g;
+  int64_t t;
+  if (tile < (int64_t)rem * t1) {
+    g = (int)(tile / t1);
+    t = tile - (int64_t)g * t1;
+  } else {
+    const int64_t x = tile - (int64_t)rem * t1;
+    g = rem + (int)(x / t0);
+    t = x - (int64_t)(g - rem) * t0;
+  }
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
+  double* Ys = reinterpret_cast<double*>(smem_raw + 64);
+  double* Us = Ys + (int64_t)ldy * b;
+  const unsigned ybytes = (unsigned)((int64_t)ldy * b * 8);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    bulk_load(Ys, a.Y + tile * (int64_t)ldy * b, ybytes, bar);
+  }
+  for (int idx = threadIdx.x; idx < b * KP; idx += kApplyNT) Us[idx] = a.u[tile * (int64_t)b * KP + idx];
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const int64_t n_g = pl.count(g);
+  const int64_t ia = pl.start(g) + t * ni;
+  const int nsl = (int)min64(ni, n_g - t * ni);
+  const int rows = nsl * rs;
+  const bool head = (t == 0);
+  const double* z0 = a.z0 + (int64_t)g * b * k;
+  const int rblk = ldy / 4, cblk = KP / 4;
+  for (int blk = threadIdx.x; blk < rblk * cblk; blk += kApplyNT) {
+    const int r0 = (blk % rblk) * 4, c0 = (blk / rblk) * 4;
+    if (r0 >= rows) continue;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = (head && r0 + u < b && c0 + v < k) ? z0[r0 + u + b * (c0 + v)] : 0.0;
+#pragma unroll 2
+    for (int l = 0; l < b; ++l) {
+      const double2 y01 = *reinterpret_cast<const double2*>(&Ys[r0 + ldy * l]);
+      const double2 y23 = *reinterpret_cast<const double2*>(&Ys[r0 + 2 + ldy * l]);
+      const double2 u01 = *reinterpret_cast<const double2*>(&Us[l * KP + c0]);
+      const double2 u23 = *reinterpret_cast<const double2*>(&Us[l * KP + c0 + 2]);
+      const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+      const double uv[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(-yv[u], uv[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u;
       if (r >= rows) continue;
-      const int c0 = cg * kApplyCW;
-      const int nc = min(kApplyCW, k - c0);
-      double acc[kApplyCW];
-#pragma unroll
-      for (int cc = 0; cc < kApplyCW; ++cc)
-        acc[cc] = (head && r < b && cc < nc) ? sm.Z[r + kApplyBM * (c0 + cc)] : 0.0;
-      for (int l = 0; l < b; ++l) {
-        const double y = Y[r + (int64_t)ldy * l];
-#pragma unroll
-        for (int cc = 0; cc < kApplyCW; ++cc)
-          if (cc < nc) acc[cc] = fma(-y, sm.U[l + kApplyBM * (c0 + cc)], acc[cc]);
-      }
       int si, w;
       tile_row(a.out.trans, r, nsl, rs, si, w);
 #pragma unroll
-      for (int cc = 0; cc < kApplyCW; ++cc)
-        if (cc < nc) a.out.base[a.out.addr(w, ia + si, c0 + cc)] = acc[cc];
+      for (int v = 0; v < 4; ++v)
+        if (c0 + v < k) a.out.base[a.out.addr(w, ia + si, c0 + v)] = acc[u][v];
     }
-    if (!head) {
-      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-        const int i = idx % b, c = idx / b;
-        sm.Z[i + kApplyBM * c] -= sm.U[i + kApplyBM * c];
-      }
-    }
-    __syncthreads();
   }
 }
-
 // ------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------
@@ -272,14 +380,18 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   cudaStream_t st = ctx.stream;
   auto leaf = tsqr_leaf_kernel<LC_>;
   set_smem_attr<LC_>((const void*)leaf);
+  {
+  ProfScope ps("tsqr_leaf", st);
   leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
   TTB_LAUNCHED();
+  }
   auto tree = tsqr_tree_kernel<TC_>;
   set_smem_attr<TC_>((const void*)tree);
   const double* rin = f.Rleaf;
   int n_in = f.plan.G;
   for (int L = 0; L < f.nloc; ++L) {
     int nodes = (n_in + f.ftree - 1) / f.ftree;
+    ProfScope ps("tsqr_tree", st);
     tree<<<nodes, TC_::NT, tile_smem<TC_>(), st>>>(rin, n_in, f.b, f.ftree, f.locY[L], f.locT[L], f.locR[L]);
     TTB_LAUNCHED();
     rin = f.locR[L];
@@ -293,7 +405,8 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     n_in = ctx.nranks;
     for (int L = 0; L < f.nglob; ++L) {
       int nodes = (n_in + f.ftree - 1) / f.ftree;
-      tree<<<nodes, TC_::NT, tile_smem<TC_>(), st>>>(rin, n_in, f.b, f.ftree, f.gloY[L], f.gloT[L], f.gloR[L]);
+      ProfScope ps("tsqr_tree", st);
+    tree<<<nodes, TC_::NT, tile_smem<TC_>(), st>>>(rin, n_in, f.b, f.ftree, f.gloY[L], f.gloT[L], f.gloR[L]);
       TTB_LAUNCHED();
       rin = f.gloR[L];
       n_in = nodes;
@@ -339,7 +452,8 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   // pivot order) and the head tile always reaches b rows.
   const int64_t min_sl = std::max<int64_t>((b + rs - 1) / rs, 2 * (int64_t)f.plan.ni);
   int64_t gmax = ns >= min_sl ? ns / min_sl : 1;
-  int G = (int)std::min<int64_t>((int64_t)2 * ctx.num_sms, std::max<int64_t>(1, gmax));
+  static const int cps = getenv("TTB_LEAF_CPS") ? atoi(getenv("TTB_LEAF_CPS")) : 2;
+  int G = (int)std::min<int64_t>((int64_t)cps * ctx.num_sms, std::max<int64_t>(1, gmax));
   if (ns == 0) G = 1;
   f.plan.G = G;
   f.ftree = MT / b;
@@ -366,18 +480,19 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   const int64_t bb = (int64_t)b * b;
   size_t total = 0;
   auto add = [&](int64_t cnt) { size_t off = total; total += ((size_t)cnt * 8 + 255) / 256 * 256; return off; };
-  size_t oY = add(ntiles * MC * b), oT = add(ntiles * bb), oRl = add((int64_t)G * bb);
+  const int64_t tsz = (bb + 1) & ~1LL;
+  size_t oY = add(ntiles * MC * b), oT = add(ntiles * tsz), oRl = add((int64_t)G * bb);
   size_t oLY[kMaxLevels], oLT[kMaxLevels], oLR[kMaxLevels];
   for (int L = 0; L < f.nloc; ++L) {
     oLY[L] = add((int64_t)nodes_loc[L] * MT * b);
-    oLT[L] = add((int64_t)nodes_loc[L] * bb);
+    oLT[L] = add((int64_t)nodes_loc[L] * tsz);
     oLR[L] = add((int64_t)nodes_loc[L] * bb);
   }
   size_t oGS = add((int64_t)ctx.nranks * bb);
   size_t oGY[kMaxLevels], oGT[kMaxLevels], oGR[kMaxLevels];
   for (int L = 0; L < f.nglob; ++L) {
     oGY[L] = add((int64_t)nodes_glo[L] * MT * b);
-    oGT[L] = add((int64_t)nodes_glo[L] * bb);
+    oGT[L] = add((int64_t)nodes_glo[L] * tsz);
     oGR[L] = add((int64_t)nodes_glo[L] * bb);
   }
   size_t oD = add(b), oR = add(bb);
@@ -408,27 +523,81 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   TTB_CHECK(k >= 1 && k <= kApplyKM, TTB_ERR_CAPABILITY, "TSQR apply: k must be in [1, 64]");
   TTB_CHECK(out.rs() == f.plan.rs && out.I == f.plan.nslices && out.ncols() == k, TTB_ERR_SHAPE,
             "TSQR apply: output view does not match the factored panel");
-  ApplyArgs a;
-  a.plan = f.plan;
-  a.ldy = f.ldy;
-  a.Y = f.Y;
-  a.T = f.T;
-  a.local.nlev = f.nloc;
-  for (int L = 0; L < f.nloc; ++L) a.local.lev[L] = Level{f.locY[L], f.locT[L], f.ldy_tree, f.ftree, -1};
-  a.global.nlev = ctx.nranks > 1 ? f.nglob : 0;
-  for (int L = 0; L < a.global.nlev; ++L) a.global.lev[L] = Level{f.gloY[L], f.gloT[L], f.ldy_tree, f.ftree, -1};
-  a.rank = ctx.rank;
-  a.z0 = z;
-  a.k = k;
-  a.D = f.D;
-  a.out = out;
+  const int b = f.b, KP = kpad(k), G = f.plan.G;
+  const int64_t bk = (int64_t)b * k, ntiles = f.plan.total_tiles();
+  // node counts per level
+  std::vector<int> lnodes(f.nloc), gnodes(ctx.nranks > 1 ? f.nglob : 0);
+  for (int L = 0, n = G; L < f.nloc; ++L) lnodes[L] = n = (n + f.ftree - 1) / f.ftree;
+  for (int L = 0, n = ctx.nranks; L < (int)gnodes.size(); ++L) gnodes[L] = n = (n + f.ftree - 1) / f.ftree;
+  int64_t maxlev = 1;
+  for (int L = 0; L < f.nloc; ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)lnodes[L] * f.ftree);
+  for (size_t L = 0; L < gnodes.size(); ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)gnodes[L] * f.ftree);
+  const int64_t nscr = 2 * maxlev * bk + ntiles * b * KP + (int64_t)G * bk;
+  double* scr = (double*)ctx.alloc((size_t)nscr * sizeof(double));
+  double* lev[2] = {scr, scr + maxlev * bk};
+  double* ubuf = scr + 2 * maxlev * bk;
+  double* z0buf = ubuf + ntiles * b * KP;
   static bool attr = false;
   if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem)));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_tree_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  tsqr_apply_kernel<<<f.plan.G, kApplyNT, sizeof(ApplySmem), ctx.stream>>>(a);
+  const double* cur = z;
+  const double* Dp = f.D;
+  int which = 0;
+  const size_t tsmem = (size_t)(3 * bk + 2 * (int64_t)b * b) * sizeof(double);
+  // global levels (redundant on every rank), then this rank's block
+  for (int L = (int)gnodes.size() - 1; L >= 0; --L) {
+    const int below = L == 0 ? ctx.nranks : gnodes[L - 1];
+    Level lv{f.gloY[L], f.gloT[L], f.ldy_tree, f.ftree, -1};
+    ProfScope ps("apply_tree", ctx.stream);
+    tsqr_tree_apply_kernel<<<gnodes[L], kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
+    TTB_LAUNCHED();
+    Dp = nullptr;
+    cur = lev[which] + (L == 0 ? (int64_t)ctx.rank * bk : 0);
+    which ^= 1;
+  }
+  for (int L = f.nloc - 1; L >= 0; --L) {
+    const int below = L == 0 ? G : lnodes[L - 1];
+    Level lv{f.locY[L], f.locT[L], f.ldy_tree, f.ftree, -1};
+    ProfScope ps("apply_tree", ctx.stream);
+    tsqr_tree_apply_kernel<<<lnodes[L], kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
+    TTB_LAUNCHED();
+    Dp = nullptr;
+    cur = lev[which];
+    which ^= 1;
+  }
+  ChainArgs ca;
+  ca.plan = f.plan;
+  ca.ldy = f.ldy;
+  ca.Y = f.Y;
+  ca.T = f.T;
+  ca.zin = cur;
+  ca.D = Dp;
+  ca.k = k;
+  ca.u = ubuf;
+  ca.z0 = z0buf;
+  const size_t csmem = 64 + (size_t)(3 * ((bk + 1) & ~1LL) + 2 * tstride_of(b)) * sizeof(double);
+  {
+  ProfScope ps("apply_chain", ctx.stream);
+  tsqr_chain_kernel<<<G, kApplyNT, csmem, ctx.stream>>>(ca);
   TTB_LAUNCHED();
+  }
+  ProductArgs pa;
+  pa.plan = f.plan;
+  pa.ldy = f.ldy;
+  pa.Y = f.Y;
+  pa.u = ubuf;
+  pa.z0 = z0buf;
+  pa.k = k;
+  pa.out = out;
+  const size_t psmem = 64 + (size_t)((int64_t)f.ldy * b + (int64_t)b * KP) * sizeof(double);
+  ProfScope ps("apply_product", ctx.stream);
+  tsqr_product_kernel<<<(unsigned)ntiles, kApplyNT, psmem, ctx.stream>>>(pa);
+  TTB_LAUNCHED();
+  ctx.free(scr);
 }
 
 void tsqr_release(Ctx& ctx, Tsqr& f) {
@@ -437,3 +606,9 @@ void tsqr_release(Ctx& ctx, Tsqr& f) {
 }
 
 }  // namespace ttb
+
+#ifdef TTB_DEBUG_CLK
+extern "C" int ttb_dbg_clk(long long* out) {
+  return cudaMemcpyFromSymbol(out, ttb::g_dclk, sizeof(long long) * 8 * 64 * 8) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -35,15 +35,24 @@ struct TCfg {
   static constexpr int NT = NW * 32;
   static constexpr int BMAX = NW * LC * CPL;
   static constexpr int MC = LR * RPL;
+  static_assert(RPL % 2 == 0, "rows come in pairs (128-bit vector loads)");
+  // tile row of register slot s in lane-row lr: consecutive pairs per lane
+  __device__ __forceinline__ static int row(int s, int lr) { return (s >> 1) * (2 * LR) + 2 * lr + (s & 1); }
+  // owner of column j: warp j % NW, lane group (j / NW) % LC, slot j / (NW*LC)
+  __device__ __forceinline__ static int owner_warp(int j) { return j % NW; }
+  __device__ __forceinline__ static int owner_lc(int j) { return (j / NW) % LC; }
+  __device__ __forceinline__ static int owner_slot(int j) { return j / (NW * LC); }
 };
 
-// leaf (2 CTAs / SM) and tree-node (one big CTA) configurations per BMAX
-using Leaf64 = TCfg<8, 2, 4, 8>;    // b <= 64, 128-row tiles
-using Leaf32 = TCfg<8, 1, 4, 8>;    // b <= 32, 256-row tiles
-using Leaf16 = TCfg<8, 1, 2, 16>;   // b <= 16, 512-row tiles
-using Tree64 = TCfg<32, 2, 1, 16>;  // 1024 thr, 256 rows: fan-in 4 at b=64
-using Tree32 = TCfg<16, 1, 2, 16>;  // 512 thr, 512 rows: fan-in 16 at b=32
-using Tree16 = TCfg<16, 1, 1, 32>;  // 512 thr, 1024 rows: fan-in 64 at b=16
+// Leaf (2 CTAs / SM) and tree-node configurations per BMAX.  Column groups
+// of LR = 8 lanes keep the per-column reductions at 3 shuffle rounds; each
+// lane holds RPL rows x CPL columns of the register tile.
+using Leaf64 = TCfg<8, 4, 2, 16>;   // b <= 64: 128-row tiles, 32 doubles / thread
+using Leaf32 = TCfg<8, 4, 1, 16>;   // b <= 32: 128-row tiles
+using Leaf16 = TCfg<8, 2, 1, 16>;   // b <= 16: 256-row tiles
+using Tree64 = TCfg<8, 4, 2, 32>;   // 256 rows: fan-in 4 at b = 64
+using Tree32 = TCfg<8, 4, 1, 32>;   // 256 rows: fan-in 8 at b = 32
+using Tree16 = TCfg<8, 2, 1, 32>;   // 512 rows: fan-in 32 at b = 16
 
 // A row-sliced view of an F-order slab (rl, I, rr):
 //   trans == 0: V(X)    rows per slice rs = rl, columns = rr
@@ -117,18 +126,81 @@ struct TreeDesc {
 // tile QR (device)
 // ------------------------------------------------------------------------
 
+constexpr int kRing = 4;  // Householder vectors in flight between warps
+
+// Debug-only cycle stamps of the column pipeline (CTA 0, second tile):
+// build with NVCC_EXTRA=-DTTB_DEBUG_CLK, read back with ttb_dbg_clk.
+#ifdef TTB_DEBUG_CLK
+static __device__ long long g_dclk[8 * 64 * 8];
+#define TTB_DCLK(ph)                                                                     \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && gbase == b && j < 64 && threadIdx.x < 256) \
+      g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                      \
+  } while (0)
+#define TTB_DCLK2(ph)                                                                        \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gj - j) > 0 && (gj - j) <= 64 && j < 64 && threadIdx.x < 256) \
+      g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                          \
+  } while (0)
+#else
+#define TTB_DCLK(ph) \
+  do {               \
+  } while (0)
+#define TTB_DCLK2(ph) \
+  do {                \
+  } while (0)
+#endif
+
 template <class C>
 struct TileSmem {
-  double Rs[C::BMAX * C::BMAX];    // chain triangle R (col-major, ld BMAX)
-  double Gs[C::BMAX * C::BMAX];    // V^T V strict upper -> T after inversion
+  double Rs[C::BMAX * C::BMAX];      // chain triangle R (col-major, ld BMAX)
+  double Gs[C::BMAX * C::BMAX];      // V^T V strict upper -> T after inversion
   double Xs[C::BMAX * C::BMAX / 2];  // inversion scratch
-  double vbuf[2][C::MC];
+  double vring[kRing][C::MC];        // published raw columns
+  double sc[kRing][4];               // published tau, scal, beta
   double taus[C::BMAX];
+  unsigned long long full[kRing];    // raw column ready (count 1)
+  unsigned long long fulls[kRing];   // scalars ready (count 1)
+  unsigned long long empty[kRing];   // consumers -> producer (count NW)
 };
 
 template <class C>
 __device__ __forceinline__ int col_of(int t, int warp, int lc) {
-  return t * (C::NW * C::LC) + warp * C::LC + lc;
+  return (t * C::LC + lc) * C::NW + warp;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  unsigned long long st;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];\n" : "=l"(st) : "r"(smem_u32(bar)) : "memory");
+  (void)st;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// once per CTA, before the first tile (count: full 1, empty NW)
+template <class C>
+__device__ void init_ring(TileSmem<C>& sm) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.fulls[s], 1);
+      mbar_init(&sm.empty[s], C::NW);
+    }
+  }
 }
 
 // In-place T = (diag(1/tau) + striu(G))^{-1}, blocked recursive inversion.
@@ -150,7 +222,7 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
       int r = rem % s, c = rem / s;
       int a0 = q * 2 * s, c0 = a0 + s;
       double acc = 0.0;
-      for (int l = 0; l <= c; ++l) acc += sm.Gs[(a0 + r) + BM * (c0 + l)] * sm.Gs[(c0 + l) + BM * (c0 + c)];
+      for (int l = 0; l <= c; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (c0 + l)], sm.Gs[(c0 + l) + BM * (c0 + c)], acc);
       sm.Xs[idx] = acc;
     }
     __syncthreads();
@@ -160,119 +232,228 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
       int r = rem % s, c = rem / s;
       int a0 = q * 2 * s, c0 = a0 + s;
       double acc = 0.0;
-      for (int l = r; l < s; ++l) acc += sm.Gs[(a0 + r) + BM * (a0 + l)] * sm.Xs[q * s * s + l + s * c];
+      for (int l = r; l < s; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (a0 + l)], sm.Xs[q * s * s + l + s * c], acc);
       sm.Gs[(a0 + r) + BM * (c0 + c)] = -acc;
     }
     __syncthreads();
   }
 }
 
-// Householder QR of one register tile.  head: pivots are tile rows 0..b-1
-// (plain QR); otherwise pivots are rows of the chain triangle sm.Rs (the
-// stacked [R; A] factorization).  On exit: A holds the Householder vectors
-// (head: R in the upper triangle of rows < b, beta on the diagonal), sm.Gs
-// holds T, sm.Rs holds R (body) -- the caller extracts R for head tiles.
-template <class C>
-__device__ void tile_qr(double (&A)[C::RPL][C::CPL], int b, bool head, TileSmem<C>& sm) {
-  constexpr int LR = C::LR, LC = C::LC, RPL = C::RPL, CPL = C::CPL, BM = C::BMAX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ---- column pipeline with delayed scaling --------------------------------
+//
+// The owner of column j publishes the RAW updated column x (rows < j zeroed
+// for head tiles) as soon as it has applied reflector j-1, then computes the
+// reflector scalars (sigma reduction, sqrt, reciprocal) and publishes those
+// separately.  With v = scal * (x - beta e_j) (head) or v = [e_j; scal x]
+// (body), consumers compute p = x . a (and q = a_j for head tiles) while the
+// scalars are still in flight, and only then finish d = v . a and the update
+// a -= tau d v.  sqrt/div leave the column-to-column critical path.
+template <class C, bool HEAD, int OT>
+__device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j, int gj, TileSmem<C>& sm) {
+  constexpr int LR = C::LR, RPL = C::RPL, BM = C::BMAX;
+  const int lane = threadIdx.x & 31;
   const int lc = lane / LR, lr = lane % LR;
-
-  for (int j = 0; j < b; ++j) {
-    const int ow = (j / LC) % C::NW, olc = j % LC, ot = j / (C::NW * LC);
-    double* vb = sm.vbuf[j & 1];
-    if (warp == ow) {
-      // every lane group computes "its" column at slot ot; only olc is used
-      double colv[RPL];
+  const bool mine = (lc == C::owner_lc(j));
+  const int slot = gj % kRing;
+  // 1. raw column
+  if (mine) {
+    double* xb = sm.vring[slot];
 #pragma unroll
-      for (int s = 0; s < RPL; ++s) {
-        double x = 0.0;
-#pragma unroll
-        for (int t = 0; t < CPL; ++t) x = (t == ot) ? A[s][t] : x;
-        colv[s] = x;
+    for (int s = 0; s < RPL; s += 2) {
+      double x0 = A[s][OT], x1 = A[s + 1][OT];
+      if (HEAD) {
+        x0 = C::row(s, lr) < j ? 0.0 : x0;
+        x1 = C::row(s + 1, lr) < j ? 0.0 : x1;
       }
-      double sig = 0.0, aj = 0.0;
+      *reinterpret_cast<double2*>(&xb[C::row(s, lr)]) = make_double2(x0, x1);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.full[slot]);
+  TTB_DCLK2(4);
+  // 2. scalars
+  double sig0 = 0.0, sig1 = 0.0, aj = 0.0;
 #pragma unroll
-      for (int s = 0; s < RPL; ++s) {
-        const int r = s * LR + lr;
-        if (!head || r > j) sig = fma(colv[s], colv[s], sig);
-        if (head && r == j) aj = colv[s];
-      }
+  for (int s = 0; s < RPL; ++s) {
+    double x = A[s][OT];
+    if (HEAD) {
+      const int r = C::row(s, lr);
+      if (r == j) aj = x;
+      x = r > j ? x : 0.0;
+    }
+    if (s & 1) sig1 = fma(x, x, sig1); else sig0 = fma(x, x, sig0);
+  }
+  double sig = sig0 + sig1;
 #pragma unroll
-      for (int off = LR / 2; off > 0; off >>= 1) {
-        sig += __shfl_xor_sync(0xffffffffu, sig, off);
-        aj += __shfl_xor_sync(0xffffffffu, aj, off);
-      }
-      const double alpha = head ? aj : sm.Rs[j + BM * j];
-      double beta, tau, scal;
-      if (sig == 0.0) {  // reflect e_j onto -e_j: keeps tau in [1, 2] always
-        beta = -alpha; tau = 2.0; scal = 0.0;
+  for (int off = LR / 2; off > 0; off >>= 1) {
+    sig += __shfl_xor_sync(0xffffffffu, sig, off);
+    if (HEAD) aj += __shfl_xor_sync(0xffffffffu, aj, off);
+  }
+  TTB_DCLK2(5);
+  const double alpha = HEAD ? aj : sm.Rs[j + BM * j];
+  // bv: the beta used in v = scal (x - bv e_j); equals beta except for an
+  // all-zero head column, where v = e_j must come from bv = -1, scal = 1.
+  double beta, tau, scal, bv;
+  if (sig == 0.0) {  // reflect e_j onto -e_j: keeps tau in [1, 2] always
+    beta = -alpha;
+    tau = 2.0;
+    if (HEAD && alpha == 0.0) {
+      scal = 1.0; bv = -1.0;
+    } else {
+      scal = HEAD ? 0.5 / alpha : 0.0; bv = beta;
+    }
+  } else {
+    // nu = sqrt(alpha^2 + sig); beta = -sign(alpha) nu
+    // tau = (beta - alpha)/beta = 1 + |alpha|/nu ; scal = 1/(alpha - beta)
+    const double nrm = sqrt(fma(alpha, alpha, sig));
+    const double den = fabs(alpha) + nrm;
+    const double rden = 1.0 / den;
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = den / nrm;
+    scal = alpha >= 0.0 ? rden : -rden;
+    bv = beta;
+  }
+  TTB_DCLK2(6);
+  if (mine && lr == 0) {  // the owner group holds this column's sigma / alpha
+    sm.sc[slot][0] = tau;
+    sm.sc[slot][1] = scal;
+    sm.sc[slot][2] = bv;
+    sm.taus[j] = tau;
+    if (!HEAD) sm.Rs[j + BM * j] = beta;
+    mbar_arrive(&sm.fulls[slot]);
+  }
+  TTB_DCLK2(7);
+  // 3. own column becomes the stored Householder vector (R on top for head)
+  if (mine) {
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const double x = A[s][OT];
+      if (HEAD) {  // rows > j: v = scal x (x_r for r > j); row j keeps R's beta
+        const int r = C::row(s, lr);
+        A[s][OT] = r > j ? x * scal : (r == j ? beta : x);
       } else {
-        const double nrm = sqrt(fma(alpha, alpha, sig));
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      if (lc == olc) {
-#pragma unroll
-        for (int s = 0; s < RPL; ++s) {
-          const int r = s * LR + lr;
-          double v, keepv;
-          if (head) {
-            v = r < j ? 0.0 : (r == j ? 1.0 : colv[s] * scal);
-            keepv = r > j ? v : (r == j ? beta : colv[s]);
-          } else {
-            v = colv[s] * scal;
-            keepv = v;
-          }
-#pragma unroll
-          for (int t = 0; t < CPL; ++t)
-            if (t == ot) A[s][t] = keepv;
-          vb[r] = v;
-        }
-        if (lr == 0) {
-          sm.taus[j] = tau;
-          if (!head) sm.Rs[j + BM * j] = beta;
-        }
+        A[s][OT] = x * scal;
       }
     }
-    __syncthreads();
-    double vr[RPL];
+  }
+}
+
+template <class C, bool HEAD>
+__device__ __forceinline__ void publish(double (&A)[C::RPL][C::CPL], int j, int gj, TileSmem<C>& sm) {
+  static_assert(C::CPL <= 2, "slot dispatch handles CPL <= 2");
+  if (C::CPL == 1 || C::owner_slot(j) == 0) publish_slot<C, HEAD, 0>(A, j, gj, sm);
+  else publish_slot<C, HEAD, (C::CPL > 1 ? 1 : 0)>(A, j, gj, sm);
+}
+
+// finish column slot T for reflector j: a -= c x (+ head pivot-row fix)
+template <class C, bool HEAD, int T>
+__device__ __forceinline__ void update_slot(double (&A)[C::RPL][C::CPL], const double (&xr)[C::RPL], double c,
+                                            double beta, double rcoef, int k, int j, int b, int lr, TileSmem<C>& sm) {
+  if (k > j && k < b) {
 #pragma unroll
-    for (int s = 0; s < RPL; ++s) vr[s] = vb[s * LR + lr];
-    const double tau = sm.taus[j];
-    double d[CPL];
+    for (int s = 0; s < C::RPL; ++s) {
+      double a = fma(-c, xr[s], A[s][T]);
+      if (HEAD && C::row(s, lr) == j) a = fma(c, beta, a);
+      A[s][T] = a;
+    }
+    if (!HEAD && lr == 0) sm.Rs[j + C::BMAX * k] -= rcoef;
+  }
+}
+
+// Householder QR of one register tile.  HEAD: pivots are tile rows 0..b-1
+// (plain QR); otherwise pivots are rows of the chain triangle sm.Rs (the
+// stacked [R; A] factorization).  gbase: number of columns this CTA has
+// already pushed through the ring (phase bookkeeping across tiles).
+// No CTA-wide barrier per column: consumers wait on the ring's full /
+// fulls barriers, the next producer on the empty barrier (slot reuse).
+// On exit: A holds the Householder vectors (head: R in the upper triangle
+// of rows < b, beta on the diagonal), sm.Gs holds T, sm.Rs holds R (body).
+template <class C, bool HEAD>
+__device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, int gbase) {
+  constexpr int LR = C::LR, RPL = C::RPL, CPL = C::CPL, BM = C::BMAX;
+  constexpr int T1 = CPL > 1 ? 1 : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lc = lane / LR, lr = lane % LR;
+  int kk[CPL];
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) kk[t] = col_of<C>(t, warp, lc);
+
+  if (warp == C::owner_warp(0)) {
+    if (gbase >= kRing) mbar_wait(&sm.empty[gbase % kRing], ((gbase / kRing) - 1) & 1);
+    publish<C, HEAD>(A, 0, gbase, sm);
+  }
+  for (int j = 0; j < b; ++j) {
+    TTB_DCLK(0);
+    const int gj = gbase + j;
+    const int slot = gj % kRing;
+    const int nx = j + 1;
+    const bool producer = (nx < b) && (warp == C::owner_warp(nx));
+    mbar_wait(&sm.full[slot], (gj / kRing) & 1);
+    TTB_DCLK(1);
+    double xr[RPL];
+#pragma unroll
+    for (int s = 0; s < RPL; s += 2) {
+      const double2 p = *reinterpret_cast<const double2*>(&sm.vring[slot][C::row(s, lr)]);
+      xr[s] = p.x;
+      xr[s + 1] = p.y;
+    }
+    double p[CPL], q[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
-      const int k = col_of<C>(t, warp, lc);
-      double acc = 0.0;
-      if (k < b && k != j) {
+      double a0 = 0.0, a1 = 0.0, qa = 0.0;
 #pragma unroll
-        for (int s = 0; s < RPL; ++s) acc = fma(vr[s], A[s][t], acc);
-        if (!head && k > j && lr == 0) acc += sm.Rs[j + BM * k];
+      for (int s = 0; s < RPL; ++s) {
+        if (s & 1) a1 = fma(xr[s], A[s][t], a1); else a0 = fma(xr[s], A[s][t], a0);
+        if (HEAD && C::row(s, lr) == j) qa = A[s][t];
       }
-      d[t] = acc;
+      p[t] = a0 + a1;
+      q[t] = qa;
     }
 #pragma unroll
     for (int off = LR / 2; off > 0; off >>= 1) {
 #pragma unroll
-      for (int t = 0; t < CPL; ++t) d[t] += __shfl_xor_sync(0xffffffffu, d[t], off);
-    }
-#pragma unroll
-    for (int t = 0; t < CPL; ++t) {
-      const int k = col_of<C>(t, warp, lc);
-      if (k > j && k < b) {
-        const double coef = tau * d[t];
-#pragma unroll
-        for (int s = 0; s < RPL; ++s) A[s][t] = fma(-coef, vr[s], A[s][t]);
-        if (!head && lr == 0) sm.Rs[j + BM * k] -= coef;
-      } else if (k < j && lr == 0) {
-        sm.Gs[k + BM * j] = d[t];
+      for (int t = 0; t < CPL; ++t) {
+        p[t] += __shfl_xor_sync(0xffffffffu, p[t], off);
+        if (HEAD) q[t] += __shfl_xor_sync(0xffffffffu, q[t], off);
       }
     }
+    if (producer && gj + 1 >= kRing) mbar_wait(&sm.empty[(gj + 1) % kRing], (((gj + 1) / kRing) - 1) & 1);
+    mbar_wait(&sm.fulls[slot], (gj / kRing) & 1);
+    TTB_DCLK(2);
+    const double tau = sm.sc[slot][0], scal = sm.sc[slot][1], beta = sm.sc[slot][2];
+    double rjk[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) rjk[t] = (!HEAD && kk[t] > j && kk[t] < b) ? sm.Rs[j + BM * kk[t]] : 0.0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    double d[CPL], c[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      // d = v . a  (head: scal (x.a - beta a_j); body: R[j,k] + scal x.a)
+      d[t] = HEAD ? scal * fma(-beta, q[t], p[t]) : fma(scal, p[t], rjk[t]);
+      c[t] = tau * d[t] * scal;
+    }
+    const int tn = producer ? C::owner_slot(nx) : -1;
+    if (producer) {
+      if (tn == 0) update_slot<C, HEAD, 0>(A, xr, c[0], beta, tau * d[0], kk[0], j, b, lr, sm);
+      else update_slot<C, HEAD, T1>(A, xr, c[T1], beta, tau * d[T1], kk[T1], j, b, lr, sm);
+      publish<C, HEAD>(A, nx, gj + 1, sm);
+      TTB_DCLK(3);
+    }
+    if (tn != 0) update_slot<C, HEAD, 0>(A, xr, c[0], beta, tau * d[0], kk[0], j, b, lr, sm);
+    if (CPL > 1 && tn != 1) update_slot<C, HEAD, T1>(A, xr, c[T1], beta, tau * d[T1], kk[T1], j, b, lr, sm);
+#pragma unroll
+    for (int t = 0; t < CPL; ++t)
+      if (kk[t] < j && lr == 0) sm.Gs[kk[t] + BM * j] = d[t];
   }
   __syncthreads();
   build_T<C>(sm, b);
+}
+
+template <class C>
+__device__ __forceinline__ void tile_qr(double (&A)[C::RPL][C::CPL], int b, bool head, TileSmem<C>& sm, int gbase) {
+  if (head) tile_qr_t<C, true>(A, b, sm, gbase);
+  else tile_qr_t<C, false>(A, b, sm, gbase);
 }
 
 template <class C>
@@ -291,7 +472,7 @@ __device__ void store_Y(const double (&A)[C::RPL][C::CPL], int b, bool head, dou
     if (k >= b) continue;
 #pragma unroll
     for (int s = 0; s < C::RPL; ++s) {
-      const int r = s * C::LR + lr;
+      const int r = C::row(s, lr);
       double v = A[s][t];
       if (head) v = r < k ? 0.0 : (r == k ? 1.0 : v);
       Y[r + (int64_t)ldy * k] = v;
@@ -318,7 +499,7 @@ __device__ void extract_R(const double (&A)[C::RPL][C::CPL], int b, TileSmem<C>&
     if (k >= b) continue;
 #pragma unroll
     for (int s = 0; s < C::RPL; ++s) {
-      const int r = s * C::LR + lr;
+      const int r = C::row(s, lr);
       if (r < b) sm.Rs[r + C::BMAX * k] = (r <= k) ? A[s][t] : 0.0;
     }
   }
