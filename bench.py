@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""TT-rounding benchmark (BASELINE.json metric "TT-rounding core GB/s").
+
+Workload (BASELINE.json configs[2], the 2 GB-class tensor the metric and the
+north-star target are quoted on): Y random TT, d=10, n=8000 per mode,
+ranks 30, fp64 N(0,1) (seeded, generated on the device); X = Y + Y (ranks
+60, 1.85 GB of cores, built by our add kernel outside the timed region);
+one step = round_tt(X, RoundingOptions(1e-10, "LRLI")) -> ranks 30.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched with torchrun; every rank holds its block_bounds slices of
+every core (the paper's 1 x P x 1 distribution) and the value is the whole
+tensor's algorithmic bytes over the max-over-ranks step time.
+
+value       = B_alg / t_step, B_alg = 8 (2|X| + |Y_out|)
+e2e         = same metric through the public API from pinned host buffers
+              (H2D of X, round_tt, D2H of the result inside the timed step)
+roofline    = dominant kernel class (TSQR leaf factorization), fp64-bound:
+              reference Householder flops / its CUDA-event time, against the
+              measured fp64 peak of this device (ttb_fp64_peak)
+cpu_baseline= the CPU restatement of the reference (oracle/, numpy + scipy
+              LAPACK, all host threads) on the same X, rank 0 only
+--impl reference: that CPU path alone, on a bounded sample of the workload
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_PEAK_FALLBACK = 6545.6  # GB/s, MEASURED_PEAKS.json hbm_gbs at round start
+
+CONFIGS = {
+    # name: (dims, Y ranks, how X is formed, eps0, max_rank)
+    "cfg1": ((2000,) * 8, 10, "y+y", 1e-10, None),
+    "cfg3": ((8000,) * 10, 30, "y+y", 1e-10, None),
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+def chain(cfg):
+    dims, r, _, _, _ = CONFIGS[cfg]
+    N = len(dims)
+    ry = (1,) + (r,) * (N - 1) + (1,)
+    rx = (1,) + (2 * r,) * (N - 1) + (1,)
+    return dims, ry, rx
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def make_input(T, comm, cfg, seed=0):
+    """Device-generated Y (seeded N(0,1), this rank's slices) and X = Y + Y."""
+    import torch
+
+    from paper_2011_06532_b200.tensor import f_empty
+
+    dims, ry, _ = chain(cfg)
+    g = torch.Generator(device=comm.device)
+    slabs = []
+    for n, d in enumerate(dims):
+        lo, hi = T.block_bounds(d, comm.size, comm.rank)
+        g.manual_seed(seed * 1000003 + n * 1009 + comm.rank)
+        s = f_empty(ry[n], hi - lo, ry[n + 1], comm.device)
+        s.normal_(generator=g)
+        slabs.append(s)
+    y = T.DistTTTensor(comm, dims, ry, slabs)
+    return y, T.add(y, y)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_06532_b200 as T
+    from paper_2011_06532_b200 import _lib, cost
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+        comm = T.DistComm()
+    else:
+        comm = T.SerialComm(torch.device("cuda", local))
+    cfg = args.config
+    dims, ry, rx = chain(cfg)
+    eps0, maxr = CONFIGS[cfg][3], CONFIGS[cfg][4]
+    opts = T.RoundingOptions(eps0, "LRLI", maxr)
+    y, x = make_input(T, comm, cfg)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=comm.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (also validates the result ranks)
+    out = None
+    for _ in range(max(args.warmup, 1)):
+        out = T.round_tt(x, opts)
+    torch.cuda.synchronize()
+    out_ranks = out.ranks
+    assert out_ranks == ry, f"rounding returned ranks {out_ranks}, expected {ry}"
+    del out
+
+    # timed region: inputs resident in HBM (1.85 GB of cores > 126 MB L2)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = T.round_tt(x, opts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_counter() - l0
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    del out
+    B = cost.rounding_bytes(dims, rx, ry)
+    F = cost.rounding_flops(dims, rx, ry, "LRLI")
+    value = B / (ms * 1e-3) / 1e9
+
+    # end-to-end through the public API from pinned host buffers
+    host_cores = [s.detach().cpu().pin_memory() for s in x.local]
+    h2d = sum(c.numel() * 8 for c in host_cores)
+    e2e_ms = []
+    d2h = 0
+    for it in range(args.warmup + args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        bev = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dev = [c.to(comm.device, non_blocking=True) for c in host_cores]
+        xt = T.DistTTTensor(comm, x.dims, x.ranks, dev)
+        o = T.round_tt(xt, opts)
+        res = [s.to("cpu", non_blocking=False) for s in o.local]
+        bev.record(stream)
+        torch.cuda.synchronize()
+        d2h = sum(r.numel() * 8 for r in res)
+        if it >= args.warmup:
+            e2e_ms.append(a.elapsed_time(bev))
+        del dev, xt, o, res
+    e2e_t = max_over_ranks(float(np.mean(e2e_ms)))
+    e2e = {"value": B / (e2e_t * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_t,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # dominant-kernel roofline from one instrumented (event-timed) step
+    dfma, dmma = _lib.fp64_peak(stream.cuda_stream)
+    _lib.prof_enable(True)
+    o = T.round_tt(x, opts)
+    torch.cuda.synchronize()
+    prof = _lib.prof_dump()
+    _lib.prof_enable(False)
+    del o
+    leaf_ms = prof.get("tsqr_leaf", (1, float("nan")))[1]
+    leaf_launch = prof.get("tsqr_leaf", (1, 0))[0]
+    leaf_f = cost.tsqr_leaf_flops(dims, rx, ry, "LRLI") / max(world, 1)
+    fp64_peak = max(dfma, dmma)
+    achieved = leaf_f / (leaf_ms * 1e-3) / 1e12
+    peak_hbm, peak_src = hbm_peak()
+    roofline = {"bound": "fp64", "kernel": "tsqr_leaf (Householder TSQR leaf chains)",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                "traffic": None, "peak_source": "measured fp64 (ttb_fp64_peak: DFMA %.1f, DMMA %.1f TF/s)" % (dfma, dmma),
+                "launches": leaf_launch, "ms_per_step": leaf_ms,
+                "share_of_step": leaf_ms / ms if ms else None}
+    step_roofline = {"hbm_frac": value / peak_hbm, "hbm_peak_gbs": peak_hbm, "hbm_peak_source": peak_src,
+                     "fp64_frac": (F / (ms * 1e-3) / 1e12) / fp64_peak,
+                     "kernel_ms": {k: round(v[1], 3) for k, v in prof.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_same_input(x, dims, rx, ry, eps0, maxr)
+
+    clocks = clk.summary()
+    line = {
+        "metric": "TT-rounding core GB/s",
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) TT cores generated on device)",
+        "config": {"workload": f"{cfg}: round_tt(X = Y + Y) d={len(dims)} n={dims[0]} ranks {rx[1]}->{ry[1]}, "
+                               f"tol {eps0}, LRLI", "dims": list(dims), "in_ranks": list(rx),
+                   "out_ranks": list(ry), "parallelism": f"mode-sliced P={world}",
+                   "l2": "inputs larger than L2 (X = %.2f GB of cores)" % (sum(cost.core_sizes(dims, rx)) * 8 / 1e9),
+                   "algorithmic_bytes": B, "algorithmic_flops": F},
+        "e2e": e2e,
+        "gpu_launches": int(launches // max(args.steps, 1)) if args.steps else 0,
+        "gpu_launches_total": int(launches),
+        "roofline": roofline,
+        "step_roofline": step_roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_same_input(x, dims, rx, ry, eps0, maxr):
+    """The CPU restatement of the reference (oracle/) on the same X, all host
+    threads; one step (~15 s on 8 cores for cfg3)."""
+    from oracle import tt_oracle as O
+
+    cores = [np.asfortranarray(s.detach().cpu().numpy()) for s in x.local]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    out, meta = O.round_tt(cores, eps0, "LRLI", maxr)
+    dt = time.perf_counter() - t0
+    from paper_2011_06532_b200 import cost
+
+    B = cost.rounding_bytes(dims, rx, ry)
+    assert O.ranks_of(out) == tuple(ry)
+    return {"value": B / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"the full workload, 1 step ({dt:.1f} s): oracle.round_tt (numpy+scipy LAPACK/OpenBLAS, "
+                      f"{threads} threads) on the same X copied to host"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU path alone
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    from oracle import tt_oracle as O
+    from paper_2011_06532_b200 import cost
+
+    cfg = args.config
+    dims, ry, rx = chain(cfg)
+    eps0, maxr = CONFIGS[cfg][3], CONFIGS[cfg][4]
+    # bounded sample: shrink the mode size so the whole run stays within ~3 min
+    budget_s = 150.0 / max(1, args.steps + args.warmup)
+    n_full = dims[0]
+    # ~16 s for the full cfg3 rounding on 8 cores; scale by core count
+    est_full = (16.0 * 8.0 / (os.cpu_count() or 8)) if cfg == "cfg3" else 0.5
+    n = int(max(200, min(n_full, n_full * budget_s / max(est_full, 1e-3))))
+    sdims = (n,) * len(dims)
+    y = O.random_cores(sdims, ry, 0) if n * ry[1] ** 2 < 5e7 else None
+    if y is None:
+        rng = np.random.default_rng(0)
+        y = [np.asfortranarray(rng.standard_normal((ry[k], d, ry[k + 1]))) for k, d in enumerate(sdims)]
+    x = O.add(y, y)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out, meta = O.round_tt(x, eps0, "LRLI", maxr)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    assert O.ranks_of(out) == tuple(ry)
+    B = cost.rounding_bytes(sdims, rx, ry)
+    t = float(np.mean(times))
+    value = B / t / 1e9
+    threads = os.cpu_count() or 1
+    line = {
+        "impl": "reference",
+        "metric": "TT-rounding core GB/s",
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) TT cores)",
+        "config": {"workload": f"{cfg}: round_tt(X = Y + Y) d={len(dims)} n={dims[0]} ranks {rx[1]}->{ry[1]}, "
+                               f"tol {eps0}, LRLI; CPU sample n={n}", "dims": list(sdims), "in_ranks": list(rx),
+                   "out_ranks": list(ry)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"mode size {n} of {n_full} (same d, ranks, tol), oracle.round_tt "
+                                   f"(numpy + scipy LAPACK/OpenBLAS, {threads} threads), mean of {args.steps} steps"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
