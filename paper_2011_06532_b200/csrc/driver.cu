@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ops.cuh"
+#include "prof.cuh"
 #include "svd.cuh"
 
 struct ttb_tsqr {
@@ -90,9 +91,10 @@ static void svd_of_rt(Ctx& ctx, const double* R, int b, double eps, int max_rank
   o.dinfo = o.s + b;
   o.info = (int*)(o.dinfo + 1);
   jacobi_svd(ctx, R, b, b, b, true, eps, max_rank, o.C, o.Vk, o.s, o.info, o.dinfo);
-  int hinfo[3] = {0, 0, 0};
-  TTB_CUDA(cudaMemcpyAsync(hinfo, o.info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  int hinfo[4] = {0, 0, 0, 0};
+  TTB_CUDA(cudaMemcpyAsync(hinfo, o.info, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   ctx.sync();
+  prof_note("svd_sweeps", hinfo[3]);
   TTB_CHECK(hinfo[2] == 0, TTB_ERR_NUMERIC, "non-finite entries in SVD input");
   o.keep = hinfo[0];
   o.capped = hinfo[1];

@@ -22,6 +22,15 @@ std::vector<Rec> open;
 
 bool prof_on() { return enabled; }
 
+namespace {
+std::vector<std::pair<std::string, double>> notes;
+}
+
+void prof_note(const char* name, double value) {
+  std::lock_guard<std::mutex> lk(mu);
+  if (enabled) notes.emplace_back(name, value);
+}
+
 void prof_record(const char* name, cudaStream_t st, bool begin) {
   std::lock_guard<std::mutex> lk(mu);
   cudaEvent_t e;
@@ -68,6 +77,12 @@ extern "C" int ttb_prof_dump(char* buf, long long cap) {
     cudaEventDestroy(r.b);
   }
   recs.clear();
+  for (auto& n : notes) {
+    if (!agg.count(n.first)) order.push_back(n.first);
+    agg[n.first].first += 1;
+    agg[n.first].second += n.second;
+  }
+  notes.clear();
   std::string out;
   for (auto& n : order) {
     char line[256];

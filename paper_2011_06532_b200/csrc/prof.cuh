@@ -8,6 +8,8 @@ namespace ttb {
 
 bool prof_on();
 void prof_record(const char* name, cudaStream_t st, bool begin);
+// non-timing counter shown by ttb_prof_dump (e.g. Jacobi sweeps)
+void prof_note(const char* name, double value);
 
 struct ProfScope {
   const char* name;

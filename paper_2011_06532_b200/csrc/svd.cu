@@ -22,11 +22,19 @@ namespace ttb {
 
 constexpr int kSvdNT = 256;
 constexpr int kSvdMax = 64;
+constexpr int kLd = kSvdMax + 1;  // padded column stride: distinct columns start on distinct banks
 constexpr int kGrp = 8;  // threads per column pair
 
+#ifdef TTB_DEBUG_CLK
+static __device__ long long g_sclk[64 * 4];
+#define SVD_CLK(ph) do { if (threadIdx.x == 0 && sweep == 0 && round < 64) g_sclk[round * 4 + (ph)] = clock64(); } while (0)
+#else
+#define SVD_CLK(ph) do {} while (0)
+#endif
+
 struct SvdSmem {
-  double A[kSvdMax * kSvdMax];   // ld = kSvdMax
-  double V[kSvdMax * kSvdMax];
+  double A[kLd * kSvdMax];   // ld = kLd
+  double V[kLd * kSvdMax];
   double sig[kSvdMax];
   int order[kSvdMax];
   int slot[kSvdMax];             // tournament position -> column
@@ -54,12 +62,12 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   if (tid == 0) sm.bad = 0;
   __syncthreads();
   for (int idx = tid; idx < kSvdMax * np; idx += kSvdNT) {
-    const int r = idx % kSvdMax, c = idx / kSvdMax;
+    const int r = idx % kSvdMax, c = idx / kSvdMax;  // rows beyond m stay zero
     double v = 0.0;
     if (r < m && c < n) v = transA ? Ain[c + (int64_t)lda * r] : Ain[r + (int64_t)lda * c];
     if (!isfinite(v)) { sm.bad = 1; v = 0.0; }
-    sm.A[r + kSvdMax * c] = v;
-    sm.V[r + kSvdMax * c] = (r == c && c < n) ? 1.0 : 0.0;
+    sm.A[r + kLd * c] = v;
+    sm.V[r + kLd * c] = (r == c && c < n) ? 1.0 : 0.0;
   }
   for (int c = tid; c < np; c += kSvdNT) sm.slot[c] = c;
   __syncthreads();
@@ -67,11 +75,14 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   const int grp = tid / kGrp, gl = tid % kGrp;
   const int npairs = np / 2;
   const double tol = 4.0 * 2.220446049250313e-16 * sqrt((double)m);
+  const double tol2 = tol * tol;
+  int sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) sm.rotated = 0;
     __syncthreads();
     for (int round = 0; round < np - 1; ++round) {
       // pair grp: slots (grp, np-1-grp) of the current tournament table
+      SVD_CLK(0);
       for (int pr = grp; pr < npairs; pr += kSvdNT / kGrp) {
         // circle-method round robin: player np-1 fixed, the rest rotate
         const int M1 = np - 1;
@@ -79,8 +90,8 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
         int q = pr == 0 ? round : (round - pr + M1) % M1;
         if (p > q) { int t = p; p = q; q = t; }
         if (q < n) {
-          double* ap = sm.A + kSvdMax * p;
-          double* aq = sm.A + kSvdMax * q;
+          double* ap = sm.A + kLd * p;
+          double* aq = sm.A + kLd * q;
           double al = 0.0, be = 0.0, ga = 0.0;
           for (int r = gl; r < m; r += kGrp) {
             const double x = ap[r], y = aq[r];
@@ -88,21 +99,25 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
             be = fma(y, y, be);
             ga = fma(x, y, ga);
           }
+          SVD_CLK(1);
           al = grp_sum(al);
           be = grp_sum(be);
           ga = grp_sum(ga);
-          if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          SVD_CLK(2);
+          if (ga != 0.0 && ga * ga > tol2 * al * be) {
+            // Rutishauser: zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))
             const double zeta = (be - al) / (2.0 * ga);
             const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+            const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
+            SVD_CLK(3);
             for (int r = gl; r < m; r += kGrp) {
               const double x = ap[r], y = aq[r];
               ap[r] = cs * x - sn * y;
               aq[r] = sn * x + cs * y;
             }
-            double* vp = sm.V + kSvdMax * p;
-            double* vq = sm.V + kSvdMax * q;
+            double* vp = sm.V + kLd * p;
+            double* vq = sm.V + kLd * q;
             for (int r = gl; r < n; r += kGrp) {
               const double x = vp[r], y = vq[r];
               vp[r] = cs * x - sn * y;
@@ -116,12 +131,13 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     }
     const int any = sm.rotated;
     __syncthreads();
+    ++sweeps;
     if (!any) break;
   }
   // singular values
   for (int c = tid / 32; c < n; c += kSvdNT / 32) {
     double acc = 0.0;
-    for (int r = tid % 32; r < m; r += 32) acc = fma(sm.A[r + kSvdMax * c], sm.A[r + kSvdMax * c], acc);
+    for (int r = tid % 32; r < m; r += 32) acc = fma(sm.A[r + kLd * c], sm.A[r + kLd * c], acc);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if ((tid % 32) == 0) sm.sig[c] = sqrt(acc);
@@ -159,6 +175,7 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     info[0] = keep;
     info[1] = capped;
     info[2] = sm.bad;
+    info[3] = sweeps;
     dinfo[0] = sqrt(tails[keep]);
   }
   for (int k = tid; k < n; k += kSvdNT) s_out[k] = sm.sig[sm.order[k]];
@@ -166,11 +183,11 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   const int keep = info[0];
   for (int idx = tid; idx < m * keep; idx += kSvdNT) {
     const int r = idx % m, k = idx / m;
-    C[r + (int64_t)m * k] = sm.A[r + kSvdMax * sm.order[k]];
+    C[r + (int64_t)m * k] = sm.A[r + kLd * sm.order[k]];
   }
   for (int idx = tid; idx < n * keep; idx += kSvdNT) {
     const int r = idx % n, k = idx / n;
-    Vk[r + (int64_t)n * k] = sm.V[r + kSvdMax * sm.order[k]];
+    Vk[r + (int64_t)n * k] = sm.V[r + kLd * sm.order[k]];
   }
 }
 
@@ -203,3 +220,9 @@ void svd_normalize_u(Ctx& ctx, const double* C, const double* s, int m, int keep
 }
 
 }  // namespace ttb
+
+#ifdef TTB_DEBUG_CLK
+extern "C" int ttb_dbg_sclk(long long* out) {
+  return cudaMemcpyFromSymbol(out, ttb::g_sclk, sizeof(long long) * 64 * 4) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int 
   double* Z = tsm;            // b x k
   double* W = Z + b * k;      // b x k
   double* U = W + b * k;      // b x k
-  double* Vt = U + b * k;     // b x b (node rows 0..b-1)
-  double* Tm = Vt + b * b;    // b x b
+  double* Vb = U + b * k;     // b x b  (V_top, then each child block)
+  double* Tm = Vb + b * b;    // b x b
   const double* Yg = L.Y + (int64_t)q * L.ldy * b;
   const double* Tg = L.T + (int64_t)q * tstride_of(b);
   for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
@@ -186,22 +186,34 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int 
     Z[idx] = d * zin[(int64_t)q * b * k + idx];
   }
   for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
-    Vt[idx] = Yg[idx % b + (int64_t)L.ldy * (idx / b)];
+    Vb[idx] = Yg[idx % b + (int64_t)L.ldy * (idx / b)];
     Tm[idx] = Tg[idx];
   }
   __syncthreads();
-  tri_gemm(Vt, b, true, Z, W, b, k);  // W = V_top^T Z
+  tri_gemm(Vb, b, true, Z, W, b, k);  // W = V_top^T Z
   __syncthreads();
   tri_gemm(Tm, b, false, W, U, b, k);  // U = T W
   __syncthreads();
   const int cnt = min(L.f, nnodes_below - q * L.f);
-  for (int idx = threadIdx.x; idx < cnt * b * k; idx += kApplyNT) {
-    const int c = idx / (b * k), rem = idx - c * b * k;
-    const int i = rem % b, cc = rem / b;
-    double acc = (c == 0) ? Z[i + b * cc] : 0.0;
-    const double* Vc = Yg + (int64_t)c * b + i;
-    for (int l = 0; l < b; ++l) acc = fma(-Vc[(int64_t)L.ldy * l], U[l + b * cc], acc);
-    zout[((int64_t)q * L.f + c) * b * k + rem] = acc;
+  for (int c = 0; c < cnt; ++c) {
+    if (c > 0) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT)
+        Vb[idx] = Yg[(int64_t)c * b + idx % b + (int64_t)L.ldy * (idx / b)];
+      __syncthreads();
+    }
+    double* zc = zout + ((int64_t)q * L.f + c) * b * k;
+    for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+      const int i = idx % b, cc = idx / b;
+      double a0 = (c == 0) ? Z[idx] : 0.0, a1 = 0.0;
+      int l = 0;
+      for (; l + 1 < b; l += 2) {
+        a0 = fma(-Vb[i + b * l], U[l + b * cc], a0);
+        a1 = fma(-Vb[i + b * (l + 1)], U[l + 1 + b * cc], a1);
+      }
+      if (l < b) a0 = fma(-Vb[i + b * l], U[l + b * cc], a0);
+      zc[idx] = a0 + a1;
+    }
   }
 }
 
@@ -368,11 +380,11 @@ size_t tile_smem() { return sizeof(TileSmem<C>); }
 
 template <class C>
 void set_smem_attr(const void* fn) {
-  static bool done = false;  // per instantiation
-  if (!done) {
-    TTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<C>)));
-    done = true;
-  }
+  static std::vector<const void*> done;  // per kernel (configs may coincide)
+  for (const void* f : done)
+    if (f == fn) return;
+  TTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<C>)));
+  done.push_back(fn);
 }
 
 template <class LC_, class TC_>
