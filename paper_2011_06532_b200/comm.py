@@ -83,6 +83,47 @@ class SerialComm(Communicator):
     """One-rank group on the current device (ttpar SerialComm, comm.py:163-181)."""
 
 
+class HostGroup:
+    """Host-side collectives over a torch.distributed group (any backend,
+    gloo included): the harness-level exchange (gather of slabs, object
+    broadcast).  Deterministic rank-ascending reductions (comm.py:220-225)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ContractError("HostGroup needs an initialised torch.distributed process group")
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allgather_object(self, obj):
+        import torch.distributed as dist
+
+        box = [None] * self.size
+        dist.all_gather_object(box, obj, group=self.group)
+        return box
+
+    def broadcast_object(self, obj, src=0):
+        import torch.distributed as dist
+
+        box = [obj]
+        dist.broadcast_object_list(box, src=src, group=self.group)
+        return box[0]
+
+    def allreduce_sum(self, arr):
+        a = np.asarray(arr, dtype=np.float64)
+        out = np.zeros_like(a)
+        for part in self.allgather_object(a):  # rank-ascending, deterministic
+            out = out + part
+        return out
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+
 class DistComm(Communicator):
     """Rank of a torch.distributed process group, one GPU per process.
 
@@ -92,20 +133,16 @@ class DistComm(Communicator):
 
     def __init__(self, group=None, device=None):
         import torch
-        import torch.distributed as dist
 
-        if not dist.is_initialized():
-            raise ContractError("DistComm needs an initialised torch.distributed process group")
+        self.host = HostGroup(group)
         self.group = group
-        self.size = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        self.size = self.host.size
+        self.rank = self.host.rank
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         super().__init__(device)
 
     def _init_comm(self):
-        import torch.distributed as dist
-
         lib = _lib.load()
         if self.size == 1:
             _lib.check(lib.ttb_ctx_init_comm(self._ctx, 1, 0, None))
@@ -113,33 +150,18 @@ class DistComm(Communicator):
         uid = C.create_string_buffer(128)
         if self.rank == 0:
             _lib.check(lib.ttb_comm_unique_id(uid))
-        box = [bytes(uid.raw)]
-        dist.broadcast_object_list(box, src=0, group=self.group)
-        uid = C.create_string_buffer(box[0], 128)
+        raw = self.host.broadcast_object(bytes(uid.raw), src=0)
+        uid = C.create_string_buffer(raw, 128)
         _lib.check(lib.ttb_ctx_init_comm(self._ctx, self.size, self.rank, uid))
 
     def allreduce_sum(self, arr):
-        import torch
-        import torch.distributed as dist
-
-        a = np.asarray(arr, dtype=np.float64)
-        parts = self.allgather_object(a)
-        out = np.zeros_like(a)
-        for p in parts:  # rank-ascending, deterministic (comm.py:220-225)
-            out = out + p
-        return out
+        return self.host.allreduce_sum(arr)
 
     def allgather_object(self, obj):
-        import torch.distributed as dist
-
-        box = [None] * self.size
-        dist.all_gather_object(box, obj, group=self.group)
-        return box
+        return self.host.allgather_object(obj)
 
     def barrier(self):
-        import torch.distributed as dist
-
-        dist.barrier(group=self.group)
+        self.host.barrier()
 
 
 class _NullTrace:
