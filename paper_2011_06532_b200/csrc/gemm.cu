@@ -5,110 +5,140 @@
 //  gemm_small_left : out_H = F * H(X)     (F is M x K, K = r_left <= 64, N = I*r_right huge)
 //  gemm_small_right: out_V = V(X) * G     (G is K x Nn, K = r_right <= 64, Mb = r_left*I huge)
 //
-// The small matrix sits in shared memory; the big operand streams through
-// once, coalesced, and every output element is written once.
+// Both are one kernel: out(m, j) = sum_k S(m, k) B(k, j) with a small S
+// (<= 64 x 64, staged zero-padded in shared memory) and a long j range,
+// computed with warp-level fp64 MMA (mma.sync m8n8k4 f64 -- on sm_100a the
+// only fp64 tensor path; it matches the DFMA peak at ~1/16 of the issued
+// instructions).  Each warp owns 8 consecutive j and all M rows: per k-step
+// of 4 it loads one B fragment (streamed from HBM, 32-byte segments) and
+// M/8 A fragments from shared memory.  Every output element is written once.
 #include "ops.cuh"
 #include "prof.cuh"
 
 namespace ttb {
 
-constexpr int kGlNT = 256, kGlNB = 64, kGlTM = 4, kGlTN = 4;
+constexpr int kSkNT = 256;  // 8 warps
+constexpr int kSkMaxM = 64, kSkMaxK = 64;
 
-__global__ void __launch_bounds__(kGlNT) gemm_small_left_kernel(int M, int K, int64_t N, const double* __restrict__ F,
-                                                                int ldf, int transF, const double* __restrict__ H,
-                                                                double* __restrict__ out) {
-  extern __shared__ __align__(16) double gl_sm[];
-  double* Fs = gl_sm;             // M x K, ld M
-  double* Hs = Fs + M * K;        // K x NB, ld K
-  const int tid = threadIdx.x;
-  for (int e = tid; e < M * K; e += kGlNT) {
-    const int i = e % M, l = e / M;
-    Fs[e] = transF ? F[l + (int64_t)ldf * i] : F[i + (int64_t)ldf * l];
-  }
-  const int tm = (M + kGlTM - 1) / kGlTM;
-  for (int64_t j0 = (int64_t)blockIdx.x * kGlNB; j0 < N; j0 += (int64_t)gridDim.x * kGlNB) {
-    const int nb = (int)min64(kGlNB, N - j0);
-    __syncthreads();
-    for (int e = tid; e < K * nb; e += kGlNT) Hs[e] = H[(int64_t)K * j0 + e];
-    __syncthreads();
-    const int tn = (nb + kGlTN - 1) / kGlTN;
-    for (int t = tid; t < tm * tn; t += kGlNT) {
-      const int i0 = (t % tm) * kGlTM, c0 = (t / tm) * kGlTN;
-      double acc[kGlTM][kGlTN];
-#pragma unroll
-      for (int u = 0; u < kGlTM; ++u)
-#pragma unroll
-        for (int v = 0; v < kGlTN; ++v) acc[u][v] = 0.0;
-      for (int l = 0; l < K; ++l) {
-        double f[kGlTM], h[kGlTN];
-#pragma unroll
-        for (int u = 0; u < kGlTM; ++u) f[u] = (i0 + u < M) ? Fs[(i0 + u) + M * l] : 0.0;
-#pragma unroll
-        for (int v = 0; v < kGlTN; ++v) h[v] = (c0 + v < nb) ? Hs[l + K * (c0 + v)] : 0.0;
-#pragma unroll
-        for (int u = 0; u < kGlTM; ++u)
-#pragma unroll
-          for (int v = 0; v < kGlTN; ++v) acc[u][v] = fma(f[u], h[v], acc[u][v]);
-      }
-#pragma unroll
-      for (int v = 0; v < kGlTN; ++v)
-#pragma unroll
-        for (int u = 0; u < kGlTM; ++u)
-          if (i0 + u < M && c0 + v < nb) out[(i0 + u) + (int64_t)M * (j0 + c0 + v)] = acc[u][v];
-    }
-  }
+struct SkinnyArgs {
+  int M, K;           // small operand S: M x K
+  int64_t N;          // long dimension
+  const double* S;    // S(m, k) = S[m * ssm + k * ssk]
+  int64_t ssm, ssk;
+  const double* B;    // B(k, j) = B[k * bsk + j * bsj]
+  int64_t bsk, bsj;
+  double* O;          // out(m, j) = O[m * osm + j * osj]
+  int64_t osm, osj;
+};
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
-void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
-                     double* out) {
-  TTB_CHECK(M <= 64 && K <= 64, TTB_ERR_CAPABILITY, "fold: small dimension above 64");
-  if (N == 0 || M == 0) return;
-  const size_t smem = (size_t)(M * K + K * kGlNB) * sizeof(double);
-  TTB_CUDA(cudaFuncSetAttribute(gemm_small_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t blocks = std::min<int64_t>((N + kGlNB - 1) / kGlNB, (int64_t)ctx.num_sms * 4);
-  ProfScope ps("fold_left", ctx.stream);
-  gemm_small_left_kernel<<<(int)blocks, kGlNT, smem, ctx.stream>>>(M, K, N, F, ldf, transF ? 1 : 0, H, out);
-  TTB_LAUNCHED();
-}
-
-template <int NC>
-__global__ void __launch_bounds__(256) gemm_small_right_kernel(int64_t Mb, int K, int Nn, const double* __restrict__ V,
-                                                               const double* __restrict__ G, int ldg, int transG,
-                                                               double* __restrict__ out) {
-  __shared__ __align__(16) double Gs[64 * NC];  // K x NC, ld NC (row k contiguous)
-  for (int e = threadIdx.x; e < K * NC; e += 256) {
-    const int l = e / NC, c = e % NC;
-    Gs[e] = (c < Nn) ? (transG ? G[c + (int64_t)ldg * l] : G[l + (int64_t)ldg * c]) : 0.0;
+template <int MB>  // M rounded up to MB*8
+__global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
+  constexpr int LDS = kSkMaxK + 1;  // padded row stride of the staged S
+  __shared__ double Ss[MB * 8 * LDS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int KP = (a.K + 3) & ~3;
+  for (int idx = threadIdx.x; idx < MB * 8 * KP; idx += kSkNT) {
+    const int m = idx / KP, k = idx % KP;
+    Ss[m * LDS + k] = (m < a.M && k < a.K) ? a.S[m * a.ssm + k * a.ssk] : 0.0;
   }
   __syncthreads();
-  for (int64_t r = blockIdx.x * 256LL + threadIdx.x; r < Mb; r += 256LL * gridDim.x) {
-    double acc[NC];
+  const int ar = lane >> 2, ac = lane & 3;  // A fragment: row, k
+  const int bk = lane & 3, bj = lane >> 2;  // B fragment: k, column
+  const int64_t nwarps = (int64_t)gridDim.x * (kSkNT / 32);
+  for (int64_t j0 = ((int64_t)blockIdx.x * (kSkNT / 32) + warp) * 8; j0 < a.N; j0 += nwarps * 8) {
+    double acc[MB][2];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    for (int l = 0; l < K; ++l) {
-      const double v = V[r + Mb * l];
+    for (int mb = 0; mb < MB; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
+    const int64_t jb = j0 + bj;
+    const bool jin = jb < a.N;
+    // all B fragments of this 8-column group first: 16 independent loads in flight
+    double bf[kSkMaxK / 4];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = fma(v, Gs[l * NC + c], acc[c]);
+    for (int q = 0; q < kSkMaxK / 4; ++q) {
+      const int kb = 4 * q + bk;
+      bf[q] = (jin && kb < a.K) ? __ldg(&a.B[kb * a.bsk + jb * a.bsj]) : 0.0;
     }
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < Nn) out[r + Mb * c] = acc[c];
+    for (int q = 0; q < kSkMaxK / 4; ++q) {
+      if (4 * q >= KP) break;
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) dmma884(acc[mb][0], acc[mb][1], Ss[(mb * 8 + ar) * LDS + 4 * q + ac], bf[q]);
+    }
+    // D fragment: row mb*8 + lane/4, columns j0 + 2*(lane%4) + {0, 1}
+    const int orow = lane >> 2, ocol = 2 * (lane & 3);
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const int m = mb * 8 + orow;
+      if (m >= a.M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t j = j0 + ocol + h;
+        if (j < a.N) a.O[m * a.osm + j * a.osj] = acc[mb][h];
+      }
+    }
   }
 }
 
+static void launch_skinny(Ctx& ctx, const SkinnyArgs& a) {
+  TTB_CHECK(a.M <= kSkMaxM && a.K <= kSkMaxK, TTB_ERR_CAPABILITY, "fold: small dimension above 64");
+  if (a.N == 0 || a.M == 0) return;
+  const int64_t groups = (a.N + 7) / 8;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((groups + 7) / 8, (int64_t)ctx.num_sms * 8));
+  const int MB = (a.M + 7) / 8;
+  switch (MB) {
+#define TTB_SK(X) \
+  case X: skinny_dmma_kernel<X><<<blocks, kSkNT, 0, ctx.stream>>>(a); break;
+    TTB_SK(1) TTB_SK(2) TTB_SK(3) TTB_SK(4) TTB_SK(5) TTB_SK(6) TTB_SK(7) TTB_SK(8)
+#undef TTB_SK
+    default: TTB_THROW(TTB_ERR_CAPABILITY, "fold: M above 64");
+  }
+  TTB_LAUNCHED();
+}
+
+// out_H (M x N) = F (M x K) * H (K x N); H col-major ld K, out col-major ld M
+void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
+                     double* out) {
+  ProfScope ps("fold_left", ctx.stream);
+  SkinnyArgs a;
+  a.M = M;
+  a.K = K;
+  a.N = N;
+  a.S = F;
+  a.ssm = transF ? ldf : 1;  // F(i, l) = transF ? F[l + ldf*i] : F[i + ldf*l]
+  a.ssk = transF ? 1 : ldf;
+  a.B = H;
+  a.bsk = 1;
+  a.bsj = K;
+  a.O = out;
+  a.osm = 1;
+  a.osj = M;
+  launch_skinny(ctx, a);
+}
+
+// out_V (Mb x Nn) = V (Mb x K) * G (K x Nn): computed as out^T = G^T V^T
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
                       double* out) {
-  TTB_CHECK(K <= 64 && Nn <= 64, TTB_ERR_CAPABILITY, "fold: small dimension above 64");
-  if (Mb == 0 || Nn == 0) return;
-  const int blocks = (int)std::min<int64_t>((Mb + 255) / 256, (int64_t)ctx.num_sms * 8);
   ProfScope ps("fold_right", ctx.stream);
-  if (Nn <= 16)
-    gemm_small_right_kernel<16><<<blocks, 256, 0, ctx.stream>>>(Mb, K, Nn, V, G, ldg, transG ? 1 : 0, out);
-  else if (Nn <= 32)
-    gemm_small_right_kernel<32><<<blocks, 256, 0, ctx.stream>>>(Mb, K, Nn, V, G, ldg, transG ? 1 : 0, out);
-  else
-    gemm_small_right_kernel<64><<<blocks, 256, 0, ctx.stream>>>(Mb, K, Nn, V, G, ldg, transG ? 1 : 0, out);
-  TTB_LAUNCHED();
+  SkinnyArgs a;
+  a.M = Nn;
+  a.K = K;
+  a.N = Mb;
+  a.S = G;  // S(c, k) = G(k, c) = transG ? G[c + ldg*k] : G[k + ldg*c]
+  a.ssm = transG ? 1 : ldg;
+  a.ssk = transG ? ldg : 1;
+  a.B = V;  // B(k, r) = V(r, k) = V[r + Mb*k]
+  a.bsk = Mb;
+  a.bsj = 1;
+  a.O = out;  // out(c, r) = out_V(r, c) = out[r + Mb*c]
+  a.osm = Mb;
+  a.osj = 1;
+  launch_skinny(ctx, a);
 }
 
 }  // namespace ttb

@@ -92,12 +92,19 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
         if (q < n) {
           double* ap = sm.A + kLd * p;
           double* aq = sm.A + kLd * q;
+          // rows gl, gl+8, ...: fixed trip count (rows >= m are zero), loads batched
+          double xa[kSvdMax / kGrp], ya[kSvdMax / kGrp];
+#pragma unroll
+          for (int u = 0; u < kSvdMax / kGrp; ++u) {
+            xa[u] = ap[gl + kGrp * u];
+            ya[u] = aq[gl + kGrp * u];
+          }
           double al = 0.0, be = 0.0, ga = 0.0;
-          for (int r = gl; r < m; r += kGrp) {
-            const double x = ap[r], y = aq[r];
-            al = fma(x, x, al);
-            be = fma(y, y, be);
-            ga = fma(x, y, ga);
+#pragma unroll
+          for (int u = 0; u < kSvdMax / kGrp; ++u) {
+            al = fma(xa[u], xa[u], al);
+            be = fma(ya[u], ya[u], be);
+            ga = fma(xa[u], ya[u], ga);
           }
           SVD_CLK(1);
           al = grp_sum(al);
@@ -111,17 +118,23 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
             const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
             SVD_CLK(3);
-            for (int r = gl; r < m; r += kGrp) {
-              const double x = ap[r], y = aq[r];
-              ap[r] = cs * x - sn * y;
-              aq[r] = sn * x + cs * y;
+#pragma unroll
+            for (int u = 0; u < kSvdMax / kGrp; ++u) {
+              ap[gl + kGrp * u] = cs * xa[u] - sn * ya[u];
+              aq[gl + kGrp * u] = sn * xa[u] + cs * ya[u];
             }
             double* vp = sm.V + kLd * p;
             double* vq = sm.V + kLd * q;
-            for (int r = gl; r < n; r += kGrp) {
-              const double x = vp[r], y = vq[r];
-              vp[r] = cs * x - sn * y;
-              vq[r] = sn * x + cs * y;
+            double xv[kSvdMax / kGrp], yv[kSvdMax / kGrp];
+#pragma unroll
+            for (int u = 0; u < kSvdMax / kGrp; ++u) {
+              xv[u] = vp[gl + kGrp * u];
+              yv[u] = vq[gl + kGrp * u];
+            }
+#pragma unroll
+            for (int u = 0; u < kSvdMax / kGrp; ++u) {
+              vp[gl + kGrp * u] = cs * xv[u] - sn * yv[u];
+              vq[gl + kGrp * u] = sn * xv[u] + cs * yv[u];
             }
             if (gl == 0) sm.rotated = 1;
           }
