@@ -92,6 +92,11 @@ void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
 
 void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }
 
+cudaStream_t Ctx::side_stream() {
+  if (!side) TTB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  return side;
+}
+
 }  // namespace ttb
 
 using namespace ttb;
@@ -135,6 +140,7 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
   TTB_TRY_BEGIN
   if (ctx) {
     if (ctx->c.nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->c.nccl_comm);
+    if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
     delete ctx;
   }
   TTB_TRY_END

@@ -19,7 +19,9 @@ struct Ctx {
   int rank = 0;
   void* nccl_comm = nullptr;
   cudaEvent_t ev = nullptr;
+  cudaStream_t side = nullptr;  // second stream for off-critical-path work (lazily created)
 
+  cudaStream_t side_stream();
   void* alloc(size_t bytes);
   void free(void* p);
   // collectives on this->stream (nranks > 1 only)

@@ -70,6 +70,35 @@ static double global_sumsq(Ctx& ctx, int64_t n, const double* x) {
   return v;
 }
 
+// side-stream helpers: the side stream starts after everything enqueued on
+// the main stream so far; its allocations are released after the main
+// stream's next uses (event ordering, never blocking the main stream).
+static void side_begin(Ctx& ctx, Ctx& sctx) {
+  cudaEvent_t e;
+  TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TTB_CUDA(cudaEventRecord(e, ctx.stream));
+  TTB_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
+  TTB_CUDA(cudaEventDestroy(e));
+}
+
+static void side_end(Ctx& ctx, Ctx& sctx, Tsqr& f2, void* svdmem) {
+  cudaEvent_t e;
+  TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TTB_CUDA(cudaEventRecord(e, ctx.stream));      // main's use of the SVD outputs
+  TTB_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
+  TTB_CUDA(cudaEventDestroy(e));
+  tsqr_release(sctx, f2);
+  sctx.free(svdmem);
+}
+
+static void side_join(Ctx& ctx, Ctx& sctx) {
+  cudaEvent_t e;
+  TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TTB_CUDA(cudaEventRecord(e, sctx.stream));
+  TTB_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
+  TTB_CUDA(cudaEventDestroy(e));
+}
+
 struct SvdOut {
   double* C = nullptr;
   double* Vk = nullptr;
@@ -304,6 +333,8 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
 
   // ---- truncation sweep ----
   bool violated = false;
+  Ctx sctx = ctx;
+  sctx.stream = ctx.side_stream();
   if (left_first) {
     for (int n = N - 1; n >= 1; --n) {
       const int b = (int)r[n];
@@ -313,7 +344,9 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
       svd_of_rt(ctx, f2.R, b, eps, mr, so);
       const int keep = so.keep;
       violated |= so.capped != 0;
-      tsqr_apply(ctx, f2, so.Vk, keep, panel_of(out[n], keep, d[n], r[n + 1], 1));
+      // output core n = (Q2 V)^T: off the critical path, on the side stream
+      side_begin(ctx, sctx);
+      tsqr_apply(sctx, f2, so.Vk, keep, panel_of(out[n], keep, d[n], r[n + 1], 1));
       if (implicit) {
         tsqr_apply(ctx, facs[n - 1], so.C, keep, panel_of(out[n - 1], r[n - 1], d[n - 1], keep, 0));
         tsqr_release(ctx, facs[n - 1]);
@@ -322,8 +355,7 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
         gemm_small_right(ctx, Mb, b, keep, out[n - 1], so.C, b, false, scratch);
         copy_d2d(ctx, out[n - 1], scratch, Mb * keep);
       }
-      ctx.free(so.mem);
-      tsqr_release(ctx, f2);
+      side_end(ctx, sctx, f2, so.mem);
       r[n] = keep;
     }
   } else {
@@ -335,7 +367,8 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
       svd_of_rt(ctx, f2.R, b, eps, mr, so);
       const int keep = so.keep;
       violated |= so.capped != 0;
-      tsqr_apply(ctx, f2, so.Vk, keep, panel_of(out[n], r[n], d[n], keep, 0));
+      side_begin(ctx, sctx);
+      tsqr_apply(sctx, f2, so.Vk, keep, panel_of(out[n], r[n], d[n], keep, 0));
       if (implicit) {
         tsqr_apply(ctx, facs[n + 1], so.C, keep, panel_of(out[n + 1], keep, d[n + 1], r[n + 2], 1));
         tsqr_release(ctx, facs[n + 1]);
@@ -344,11 +377,11 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
         gemm_small_left(ctx, keep, b, Nb, so.C, b, true, out[n + 1], scratch);
         copy_d2d(ctx, out[n + 1], scratch, keep * Nb);
       }
-      ctx.free(so.mem);
-      tsqr_release(ctx, f2);
+      side_end(ctx, sctx, f2, so.mem);
       r[n + 1] = keep;
     }
   }
+  side_join(ctx, sctx);
   if (scratch) ctx.free(scratch);
   meta[2] = violated ? 1.0 : 0.0;
   for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
