@@ -14,7 +14,7 @@ from .errors import (CapabilityError, CapacityError, ContractError, NumericError
                      ShapeError, TTError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_ttb.so")
+SO_PATH = os.environ.get("TTB_LIB") or os.path.join(_HERE, "_ttb.so")
 
 TTB_OK = 0
 _ERRMAP = {

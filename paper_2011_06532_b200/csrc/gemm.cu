@@ -14,6 +14,7 @@
 // M/8 A fragments from shared memory.  Every output element is written once.
 #include "ops.cuh"
 #include "prof.cuh"
+#include "dmma.cuh"
 
 namespace ttb {
 
@@ -30,12 +31,6 @@ struct SkinnyArgs {
   double* O;          // out(m, j) = O[m * osm + j * osj]
   int64_t osm, osj;
 };
-
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 template <int MB>  // M rounded up to MB*8
 __global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
@@ -68,7 +63,7 @@ __global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
     for (int q = 0; q < kSkMaxK / 4; ++q) {
       if (4 * q >= KP) break;
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) dmma884(acc[mb][0], acc[mb][1], Ss[(mb * 8 + ar) * LDS + 4 * q + ac], bf[q]);
+      for (int mb = 0; mb < MB; ++mb) dmma_884(acc[mb][0], acc[mb][1], Ss[(mb * 8 + ar) * LDS + 4 * q + ac], bf[q]);
     }
     // D fragment: row mb*8 + lane/4, columns j0 + 2*(lane%4) + {0, 1}
     const int orow = lane >> 2, ocol = 2 * (lane & 3);

@@ -5,6 +5,7 @@
 #include "tsqr.cuh"
 #include "ctx.cuh"
 #include "prof.cuh"
+#include "dmma.cuh"
 
 namespace ttb {
 
@@ -147,73 +148,69 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 __host__ __device__ __forceinline__ int64_t tstride_of(int b) { return ((int64_t)b * b + 1) & ~1LL; }
 __host__ __device__ __forceinline__ int kpad(int k) { return (k + 3) & ~3; }
 
-// Out[i + b*c] = sum_{l >= i} M(i, l) In[l + b*c]; M(i,l) = vtop ? M[l + ldm*i] : M[i + ldm*l]
-__device__ __forceinline__ void tri_gemm(const double* M, int ldm, bool vtop, const double* In, double* Out, int b,
-                                         int k) {
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, c = idx / b;
-    double a0 = 0.0, a1 = 0.0;
-    int l = i;
-    for (; l + 1 < b; l += 2) {
-      const double m0 = vtop ? M[l + ldm * i] : M[i + ldm * l];
-      const double m1 = vtop ? M[l + 1 + ldm * i] : M[i + ldm * (l + 1)];
-      a0 = fma(m0, In[l + b * c], a0);
-      a1 = fma(m1, In[l + 1 + b * c], a1);
-    }
-    if (l < b) a0 = fma(vtop ? M[l + ldm * i] : M[i + ldm * l], In[l + b * c], a0);
-    Out[idx] = a0 + a1;
-  }
-}
+// shared-memory leading dimension for DMMA operand staging: >= n and
+// congruent to 4 mod 16 (in doubles), so the 4x4 lane pattern of an m8n8k4
+// fragment load (fr + ld*fc, fr, fc < 4) hits 16 distinct 8-byte banks
+__host__ __device__ __forceinline__ int ldpad(int n) { return ((n + 11) & ~15) + 4; }
 
 // ---- 1. tree levels -------------------------------------------------------
 // zin: (nodes) blocks of b x k (ld b); zout: (nodes * f) child blocks.
 // D (optional) multiplies the rows of the root input (sign fix).
+// All three products run on the fp64 MMA path (cta_dmma): W = V_top^T Z,
+// U = T W, z_c = [Z;0]_c - V_c U.
 __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int nnodes_below, int b, int k,
                                                                    const double* __restrict__ zin,
                                                                    const double* __restrict__ D,
                                                                    double* __restrict__ zout) {
   extern __shared__ __align__(16) double tsm[];
+  constexpr int NW = kApplyNT / 32;
   const int q = blockIdx.x;
-  double* Z = tsm;            // b x k
-  double* W = Z + b * k;      // b x k
-  double* U = W + b * k;      // b x k
-  double* Vb = U + b * k;     // b x b  (V_top, then each child block)
-  double* Tm = Vb + b * b;    // b x b
+  const int ld = ldpad(b);
+  double* Z = tsm;            // b x k (ld)
+  double* W = Z + ld * k;     // b x k
+  double* U = W + ld * k;     // b x k
+  double* Vb = U + ld * k;    // b x b  (V_top, then each child block)
+  double* Tm = Vb + ld * b;   // b x b
   const double* Yg = L.Y + (int64_t)q * L.ldy * b;
   const double* Tg = L.T + (int64_t)q * tstride_of(b);
   for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const double d = D ? D[idx % b] : 1.0;
-    Z[idx] = d * zin[(int64_t)q * b * k + idx];
+    const int i = idx % b, c = idx / b;
+    const double d = D ? D[i] : 1.0;
+    Z[i + ld * c] = d * zin[(int64_t)q * b * k + idx];
   }
   for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
-    Vb[idx] = Yg[idx % b + (int64_t)L.ldy * (idx / b)];
-    Tm[idx] = Tg[idx];
+    const int i = idx % b, j = idx / b;
+    Vb[i + ld * j] = Yg[i + (int64_t)L.ldy * j];
+    Tm[i + ld * j] = Tg[idx];
   }
   __syncthreads();
-  tri_gemm(Vb, b, true, Z, W, b, k);  // W = V_top^T Z
+  // W = V_top^T Z  (V_top unit lower: V_top^T(m, l) nonzero for l >= m)
+  cta_dmma(
+      b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Vb[l + ld * m] : 0.0; },
+      [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
+      [&](int m, int n, double v) { W[m + ld * n] = v; });
   __syncthreads();
-  tri_gemm(Tm, b, false, W, U, b, k);  // U = T W
-  __syncthreads();
+  // U = T W  (T upper)
+  cta_dmma(
+      b, k, b, NW, [&](int m, int l) { return (l >= m && l < b && m < b) ? Tm[m + ld * l] : 0.0; },
+      [&](int l, int n) { return (l < b && n < k) ? W[l + ld * n] : 0.0; },
+      [&](int m, int n, double v) { U[m + ld * n] = v; });
   const int cnt = min(L.f, nnodes_below - q * L.f);
   for (int c = 0; c < cnt; ++c) {
     if (c > 0) {
       __syncthreads();
-      for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT)
-        Vb[idx] = Yg[(int64_t)c * b + idx % b + (int64_t)L.ldy * (idx / b)];
-      __syncthreads();
-    }
-    double* zc = zout + ((int64_t)q * L.f + c) * b * k;
-    for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-      const int i = idx % b, cc = idx / b;
-      double a0 = (c == 0) ? Z[idx] : 0.0, a1 = 0.0;
-      int l = 0;
-      for (; l + 1 < b; l += 2) {
-        a0 = fma(-Vb[i + b * l], U[l + b * cc], a0);
-        a1 = fma(-Vb[i + b * (l + 1)], U[l + 1 + b * cc], a1);
+      for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
+        const int i = idx % b, j = idx / b;
+        Vb[i + ld * j] = Yg[(int64_t)c * b + i + (int64_t)L.ldy * j];
       }
-      if (l < b) a0 = fma(-Vb[i + b * l], U[l + b * cc], a0);
-      zc[idx] = a0 + a1;
     }
+    __syncthreads();
+    double* zc = zout + ((int64_t)q * L.f + c) * b * k;
+    const bool top = (c == 0);
+    cta_dmma(
+        b, k, b, NW, [&](int m, int l) { return (m < b && l < b) ? Vb[m + ld * l] : 0.0; },
+        [&](int l, int n) { return (l < b && n < k) ? U[l + ld * n] : 0.0; },
+        [&](int m, int n, double v) { zc[m + b * n] = (top ? Z[m + ld * n] : 0.0) - v; });
   }
 }
 
@@ -226,21 +223,25 @@ struct ChainArgs {
   const double* zin;     // per CTA b x k (ld b)
   const double* D;       // sign fix when there is no tree above (else null)
   int k;
-  double* u;             // per tile b x KP, row-major (l*KP + c)
+  double* u;             // per tile b x KP, row-major (l*KP + c); columns >= k unused
   double* z0;            // per CTA b x k: the head tile's input z_0
 };
 
+// One CTA per leaf chain, tiles in reverse.  z ping-pongs between two
+// shared buffers so that u_t = T_t z_t, z_{t-1} = z_t - u_t is one MMA pass
+// and one barrier per tile; T_t arrives by bulk copy two tiles ahead.
 __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NW = kApplyNT / 32;
   const int g = blockIdx.x;
   const LeafPlan& pl = a.plan;
-  const int b = pl.b, k = a.k, KP = kpad(k);
+  const int b = pl.b, k = a.k, KP = kpad(k), ld = ldpad(b);
   const int64_t tsz = tstride_of(b);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // T double buffer
-  double* Z = reinterpret_cast<double*>(smem_raw + 64);
-  double* U = Z + ((b * k + 1) & ~1);
-  double* W = U + ((b * k + 1) & ~1);
-  double* Tb0 = W + ((b * k + 1) & ~1);
+  double* const Zb0 = reinterpret_cast<double*>(smem_raw + 64);
+  double* const Zb1 = Zb0 + ld * k;
+  double* W = Zb1 + ld * k;
+  double* Tb0 = W + ld * k;
   double* Tb1 = Tb0 + tsz;
   const int64_t n_g = pl.count(g);
   const int ntiles = pl.tiles_of(n_g);
@@ -248,10 +249,12 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const double d = a.D ? a.D[idx % b] : 1.0;
-    Z[idx] = d * a.zin[(int64_t)g * b * k + idx];
+    const int i = idx % b, c = idx / b;
+    const double d = a.D ? a.D[i] : 1.0;
+    Zb0[i + ld * c] = d * a.zin[(int64_t)g * b * k + idx];
   }
   __syncthreads();
   const unsigned tbytes = (unsigned)(tsz * 8);
@@ -259,32 +262,43 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
     bulk_load(Tb0, a.T + (tb + ntiles - 1) * tsz, tbytes, &bars[0]);
     if (ntiles > 1) bulk_load(Tb1, a.T + (tb + ntiles - 2) * tsz, tbytes, &bars[1]);
   }
+  int zc = 0;
   for (int t = ntiles - 1, it = 0; t >= 0; --t, ++it) {
     const int cur = it & 1;
-    double* Tc = cur ? Tb1 : Tb0;
+    const double* Tc = cur ? Tb1 : Tb0;
+    const double* Z = zc ? Zb1 : Zb0;
+    double* Zn = zc ? Zb0 : Zb1;
     mbar_wait(&bars[cur], (it >> 1) & 1);
     double* ut = a.u + (tb + t) * (int64_t)b * KP;
+    auto Ta = [&](int m, int l) { return (l >= m && l < b && m < b) ? Tc[m + b * l] : 0.0; };
     if (t == 0) {
       // head: u_0 = T_0 (V_top^T z_0), V_top = rows 0..b-1 of Y_0 (global)
       const double* Y0 = a.Y + tb * (int64_t)a.ldy * b;
-      tri_gemm(Y0, a.ldy, true, Z, W, b, k);
+      cta_dmma(
+          b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Y0[l + (int64_t)a.ldy * m] : 0.0; },
+          [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
+          [&](int m, int n, double v) { W[m + ld * n] = v; });
       __syncthreads();
-      tri_gemm(Tc, b, false, W, U, b, k);
-      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) a.z0[(int64_t)g * b * k + idx] = Z[idx];
+      cta_dmma(
+          b, k, b, NW, Ta, [&](int l, int n) { return (l < b && n < k) ? W[l + ld * n] : 0.0; },
+          [&](int m, int n, double v) { ut[m * KP + n] = v; });
+      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+        const int i = idx % b, c = idx / b;
+        a.z0[(int64_t)g * b * k + idx] = Z[i + ld * c];
+      }
     } else {
-      tri_gemm(Tc, b, false, Z, U, b, k);  // U = T_t Z
+      cta_dmma(
+          b, k, b, NW, Ta, [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
+          [&](int m, int n, double v) {
+            ut[m * KP + n] = v;
+            Zn[m + ld * n] = Z[m + ld * n] - v;
+          });
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < b * KP; idx += kApplyNT) {
-      const int l = idx / KP, c = idx % KP;
-      ut[idx] = c < k ? U[l + b * c] : 0.0;
-    }
-    if (t > 0)
-      for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) Z[idx] -= U[idx];
-    __syncthreads();
+    zc ^= 1;
     if (threadIdx.x == 0 && t >= 2) {
       fence_proxy_async();
-      bulk_load(Tc, a.T + (tb + t - 2) * tsz, tbytes, &bars[cur]);
+      bulk_load(const_cast<double*>(Tc), a.T + (tb + t - 2) * tsz, tbytes, &bars[cur]);
     }
   }
 }
@@ -300,10 +314,14 @@ struct ProductArgs {
   Panel out;
 };
 
+// One CTA per tile: out_t = -Y_t u_t (+ z_0 on the head tile's top rows).
+// Y_t is bulk-copied column by column into a bank-padded shared layout.
 __global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NW = kApplyNT / 32;
   const LeafPlan& pl = a.plan;
   const int b = pl.b, k = a.k, KP = kpad(k), ldy = a.ldy, rs = pl.rs, ni = pl.ni;
+  const int lys = ldpad(ldy), ldu = ldpad(k);
   const int64_t tile = blockIdx.x;
   // tile -> (CTA g, position t) of the factor's chains
   const int rem = pl.rem();
@@ -320,14 +338,21 @@ __global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a
   }
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
   double* Ys = reinterpret_cast<double*>(smem_raw + 64);
-  double* Us = Ys + (int64_t)ldy * b;
-  const unsigned ybytes = (unsigned)((int64_t)ldy * b * 8);
+  double* Us = Ys + (int64_t)lys * b;
+  const double* Yg = a.Y + tile * (int64_t)ldy * b;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    bulk_load(Ys, a.Y + tile * (int64_t)ldy * b, ybytes, bar);
+    mbar_expect_tx(bar, (unsigned)(ldy * b * 8));
   }
-  for (int idx = threadIdx.x; idx < b * KP; idx += kApplyNT) Us[idx] = a.u[tile * (int64_t)b * KP + idx];
+  __syncthreads();
+  if (threadIdx.x < 32)
+    for (int j = threadIdx.x; j < b; j += 32) bulk_g2s(Ys + lys * j, Yg + (int64_t)ldy * j, ldy * 8, bar);
+  const double* ug = a.u + tile * (int64_t)b * KP;
+  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+    const int l = idx / k, c = idx % k;
+    Us[l * ldu + c] = ug[l * KP + c];
+  }
   __syncthreads();
   mbar_wait(bar, 0);
   const int64_t n_g = pl.count(g);
@@ -336,39 +361,15 @@ __global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a
   const int rows = nsl * rs;
   const bool head = (t == 0);
   const double* z0 = a.z0 + (int64_t)g * b * k;
-  const int rblk = ldy / 4, cblk = KP / 4;
-  for (int blk = threadIdx.x; blk < rblk * cblk; blk += kApplyNT) {
-    const int r0 = (blk % rblk) * 4, c0 = (blk / rblk) * 4;
-    if (r0 >= rows) continue;
-    double acc[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = (head && r0 + u < b && c0 + v < k) ? z0[r0 + u + b * (c0 + v)] : 0.0;
-#pragma unroll 2
-    for (int l = 0; l < b; ++l) {
-      const double2 y01 = *reinterpret_cast<const double2*>(&Ys[r0 + ldy * l]);
-      const double2 y23 = *reinterpret_cast<const double2*>(&Ys[r0 + 2 + ldy * l]);
-      const double2 u01 = *reinterpret_cast<const double2*>(&Us[l * KP + c0]);
-      const double2 u23 = *reinterpret_cast<const double2*>(&Us[l * KP + c0 + 2]);
-      const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
-      const double uv[4] = {u01.x, u01.y, u23.x, u23.y};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(-yv[u], uv[v], acc[u][v]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + u;
-      if (r >= rows) continue;
-      int si, w;
-      tile_row(a.out.trans, r, nsl, rs, si, w);
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (c0 + v < k) a.out.base[a.out.addr(w, ia + si, c0 + v)] = acc[u][v];
-    }
-  }
+  cta_dmma(
+      rows, k, b, NW, [&](int m, int l) { return (m < rows && l < b) ? Ys[m + lys * l] : 0.0; },
+      [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
+      [&](int m, int n, double v) {
+        const double base = (head && m < b) ? z0[m + b * n] : 0.0;
+        int si, w;
+        tile_row(a.out.trans, m, nsl, rs, si, w);
+        a.out.base[a.out.addr(w, ia + si, n)] = base - v;
+      });
 }
 // ------------------------------------------------------------------------
 // host side
@@ -464,7 +465,10 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   // pivot order) and the head tile always reaches b rows.
   const int64_t min_sl = std::max<int64_t>((b + rs - 1) / rs, 2 * (int64_t)f.plan.ni);
   int64_t gmax = ns >= min_sl ? ns / min_sl : 1;
-  static const int cps = getenv("TTB_LEAF_CPS") ? atoi(getenv("TTB_LEAF_CPS")) : 2;
+  // resident CTAs per SM: 2 for 256-thread leaf configurations, else 1
+  const int nt = f.cls == 16 ? Leaf16::NT : f.cls == 32 ? Leaf32::NT : Leaf64::NT;
+  static const int cps_env = getenv("TTB_LEAF_CPS") ? atoi(getenv("TTB_LEAF_CPS")) : 0;
+  const int cps = cps_env > 0 ? cps_env : (nt <= 256 ? 2 : 1);
   int G = (int)std::min<int64_t>((int64_t)cps * ctx.num_sms, std::max<int64_t>(1, gmax));
   if (ns == 0) G = 1;
   f.plan.G = G;
@@ -559,7 +563,8 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   const double* cur = z;
   const double* Dp = f.D;
   int which = 0;
-  const size_t tsmem = (size_t)(3 * bk + 2 * (int64_t)b * b) * sizeof(double);
+  const int ldb = ldpad(b);
+  const size_t tsmem = (size_t)(3 * (int64_t)ldb * k + 2 * (int64_t)ldb * b) * sizeof(double);
   // global levels (redundant on every rank), then this rank's block
   for (int L = (int)gnodes.size() - 1; L >= 0; --L) {
     const int below = L == 0 ? ctx.nranks : gnodes[L - 1];
@@ -591,7 +596,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   ca.k = k;
   ca.u = ubuf;
   ca.z0 = z0buf;
-  const size_t csmem = 64 + (size_t)(3 * ((bk + 1) & ~1LL) + 2 * tstride_of(b)) * sizeof(double);
+  const size_t csmem = 64 + (size_t)(3 * (int64_t)ldb * k + 2 * tstride_of(b)) * sizeof(double);
   {
   ProfScope ps("apply_chain", ctx.stream);
   tsqr_chain_kernel<<<G, kApplyNT, csmem, ctx.stream>>>(ca);
@@ -605,7 +610,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.z0 = z0buf;
   pa.k = k;
   pa.out = out;
-  const size_t psmem = 64 + (size_t)((int64_t)f.ldy * b + (int64_t)b * KP) * sizeof(double);
+  const size_t psmem = 64 + (size_t)((int64_t)ldpad(f.ldy) * b + (int64_t)b * ldpad(k)) * sizeof(double);
   ProfScope ps("apply_product", ctx.stream);
   tsqr_product_kernel<<<(unsigned)ntiles, kApplyNT, psmem, ctx.stream>>>(pa);
   TTB_LAUNCHED();

@@ -47,12 +47,31 @@ struct TCfg {
 // Leaf (2 CTAs / SM) and tree-node configurations per BMAX.  Column groups
 // of LR = 8 lanes keep the per-column reductions at 3 shuffle rounds; each
 // lane holds RPL rows x CPL columns of the register tile.
-using Leaf64 = TCfg<8, 4, 2, 16>;   // b <= 64: 128-row tiles, 32 doubles / thread
-using Leaf32 = TCfg<8, 4, 1, 16>;   // b <= 32: 128-row tiles
-using Leaf16 = TCfg<8, 2, 1, 16>;   // b <= 16: 256-row tiles
-using Tree64 = TCfg<8, 4, 2, 32>;   // 256 rows: fan-in 4 at b = 64
-using Tree32 = TCfg<8, 4, 1, 32>;   // 256 rows: fan-in 8 at b = 32
-using Tree16 = TCfg<8, 2, 1, 32>;   // 512 rows: fan-in 32 at b = 16
+// (TTB_LEAF64 etc. override a configuration at compile time for tuning runs)
+#ifndef TTB_LEAF64
+#define TTB_LEAF64 16, 2, 2, 16
+#endif
+#ifndef TTB_LEAF32
+#define TTB_LEAF32 8, 4, 1, 16
+#endif
+#ifndef TTB_LEAF16
+#define TTB_LEAF16 8, 2, 1, 16
+#endif
+#ifndef TTB_TREE64
+#define TTB_TREE64 8, 2, 4, 16
+#endif
+#ifndef TTB_TREE32
+#define TTB_TREE32 8, 4, 1, 32
+#endif
+#ifndef TTB_TREE16
+#define TTB_TREE16 8, 2, 1, 32
+#endif
+using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 512 threads, 1 CTA / SM
+using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 128-row tiles
+using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 256-row tiles
+using Tree64 = TCfg<TTB_TREE64>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
+using Tree32 = TCfg<TTB_TREE32>;   // 256 rows: fan-in 8 at b = 32
+using Tree16 = TCfg<TTB_TREE16>;   // 512 rows: fan-in 32 at b = 16
 
 // A row-sliced view of an F-order slab (rl, I, rr):
 //   trans == 0: V(X)    rows per slice rs = rl, columns = rr
@@ -338,11 +357,19 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
   }
 }
 
+// register-slot index clamped to the configuration (dispatch helpers)
+template <class C, int T>
+constexpr int kSlot = T < C::CPL ? T : C::CPL - 1;
+
 template <class C, bool HEAD>
 __device__ __forceinline__ void publish(double (&A)[C::RPL][C::CPL], int j, int gj, TileSmem<C>& sm) {
-  static_assert(C::CPL <= 2, "slot dispatch handles CPL <= 2");
-  if (C::CPL == 1 || C::owner_slot(j) == 0) publish_slot<C, HEAD, 0>(A, j, gj, sm);
-  else publish_slot<C, HEAD, (C::CPL > 1 ? 1 : 0)>(A, j, gj, sm);
+  static_assert(C::CPL <= 4, "slot dispatch handles CPL <= 4");
+  switch (C::owner_slot(j)) {
+    case 0: publish_slot<C, HEAD, 0>(A, j, gj, sm); break;
+    case 1: publish_slot<C, HEAD, kSlot<C, 1>>(A, j, gj, sm); break;
+    case 2: publish_slot<C, HEAD, kSlot<C, 2>>(A, j, gj, sm); break;
+    default: publish_slot<C, HEAD, kSlot<C, 3>>(A, j, gj, sm); break;
+  }
 }
 
 // finish column slot T for reflector j: a -= c x (+ head pivot-row fix)
@@ -434,14 +461,22 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       c[t] = tau * d[t] * scal;
     }
     const int tn = producer ? C::owner_slot(nx) : -1;
-    if (producer) {
-      if (tn == 0) update_slot<C, HEAD, 0>(A, xr, c[0], beta, tau * d[0], kk[0], j, b, lr, sm);
-      else update_slot<C, HEAD, T1>(A, xr, c[T1], beta, tau * d[T1], kk[T1], j, b, lr, sm);
+#define TTB_UPD(T) update_slot<C, HEAD, T>(A, xr, c[T], beta, tau * d[T], kk[T], j, b, lr, sm)
+    if (producer) {  // the next column first: it is on the critical path
+      switch (tn) {
+        case 0: TTB_UPD(0); break;
+        case 1: TTB_UPD(T1); break;
+        case 2: TTB_UPD((kSlot<C, 2>)); break;
+        default: TTB_UPD((kSlot<C, 3>)); break;
+      }
       publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
     }
-    if (tn != 0) update_slot<C, HEAD, 0>(A, xr, c[0], beta, tau * d[0], kk[0], j, b, lr, sm);
-    if (CPL > 1 && tn != 1) update_slot<C, HEAD, T1>(A, xr, c[T1], beta, tau * d[T1], kk[T1], j, b, lr, sm);
+    if (tn != 0) TTB_UPD(0);
+    if (CPL > 1 && tn != 1) TTB_UPD(T1);
+    if (CPL > 2 && tn != 2) TTB_UPD((kSlot<C, 2>));
+    if (CPL > 3 && tn != 3) TTB_UPD((kSlot<C, 3>));
+#undef TTB_UPD
 #pragma unroll
     for (int t = 0; t < CPL; ++t)
       if (kk[t] < j && lr == 0) sm.Gs[kk[t] + BM * j] = d[t];
