@@ -45,6 +45,9 @@ struct Tsqr {
   const double* Rraw = nullptr;
   double* D = nullptr;  // sign fix (b)
   double* R = nullptr;  // final sign-fixed R (b x b, col-major), replicated
+  unsigned* prog = nullptr;  // tree progress counters (one per node)
+  double* Rrow = nullptr;    // tree row streams (one b x ldr block per node)
+  int ldr = 0;
   void* mem = nullptr;
 };
 

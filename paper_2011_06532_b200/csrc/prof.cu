@@ -13,6 +13,7 @@ namespace {
 struct Rec {
   std::string name;
   cudaEvent_t a, b;
+  cudaStream_t st;
 };
 std::mutex mu;
 bool enabled = false;
@@ -37,7 +38,7 @@ void prof_record(const char* name, cudaStream_t st, bool begin) {
   cudaEventCreate(&e);
   cudaEventRecord(e, st);
   if (begin) {
-    open.push_back(Rec{name, e, nullptr});
+    open.push_back(Rec{name, e, nullptr, st});
   } else {
     for (size_t i = open.size(); i-- > 0;) {
       if (open[i].name == name) {
@@ -66,6 +67,20 @@ extern "C" int ttb_prof_dump(char* buf, long long cap) {
   std::lock_guard<std::mutex> lk(mu);
   std::vector<std::string> order;
   std::map<std::string, std::pair<long long, double>> agg;
+  // optional timeline (debugging): TTB_PROF_TIMELINE=<file>, one line per
+  // scope "name start_ms end_ms stream" relative to the first scope
+  if (const char* tl = getenv("TTB_PROF_TIMELINE")) {
+    if (FILE* fp = fopen(tl, "w")) {
+      for (auto& r : recs) {
+        cudaEventSynchronize(r.b);
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, recs[0].a, r.a);
+        cudaEventElapsedTime(&t1, recs[0].a, r.b);
+        fprintf(fp, "%s %.4f %.4f %p\n", r.name.c_str(), t0, t1, (void*)r.st);
+      }
+      fclose(fp);
+    }
+  }
   for (auto& r : recs) {
     cudaEventSynchronize(r.b);
     float ms = 0.f;

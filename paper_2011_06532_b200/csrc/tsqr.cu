@@ -9,6 +9,18 @@
 
 namespace ttb {
 
+// bulk-copy (TMA engine) helpers
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // ------------------------------------------------------------------------
 // leaf kernel: one CTA = one chain of tiles over a contiguous slice run
 // ------------------------------------------------------------------------
@@ -61,40 +73,242 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
 }
 
 // ------------------------------------------------------------------------
-// tree kernel: node q factors the stacked triangles Rin[q*f .. q*f+cnt)
+// tree kernel: every level of the reduction tree in ONE launch.  Node q of
+// level L factors the stacked triangles of its children.  Level-0 inputs
+// (the leaf triangles) are complete at launch; a node of level L >= 1 reads
+// its children's R rows as they become final: a child publishes row j of R
+// once it applied reflector j, and counts finished chunks of kTreeChunk rows
+// in a per-node progress counter.  The parent's column j only needs rows
+// <= j of every child (the support of reflector j of a stacked-triangle QR
+// is block 0's row j and rows 0..j of the other blocks), so levels run as a
+// wavefront a few columns apart instead of one after another.  All nodes
+// are co-resident (one CTA per SM, nodes < SMs); children have lower block
+// indices than their parents and never wait on them.
 // ------------------------------------------------------------------------
+struct TreePlan {
+  int nlev, b, f;
+  int first[kMaxLevels + 1];  // global node index of each level's first node
+  int n_in[kMaxLevels];       // inputs (children) of each level
+  const double* Rin[kMaxLevels];
+  double* Y[kMaxLevels];
+  double* T[kMaxLevels];
+  double* R[kMaxLevels];
+  double* Rrow;               // per node: R rows as they finalise, row-major, ld ldr
+  int ldr;
+  unsigned* prog;             // per node: NW x finished chunks (zeroed per launch)
+};
+
+constexpr int kMaxChunks = 64;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// polling load without acquire ordering (later memory operations of the
+// warp do not wait for it); a fence.acq_rel follows a successful poll
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
+  return v;
+}
+
+#if defined(TTB_TCLK2) && !defined(TTB_TCLK)
+#define TTB_TCLK
+#define TTB_TCLK_NOCHUNK
+#endif
+#ifdef TTB_TCLK
+static __device__ unsigned long long g_tclk[160 * 64];
+extern "C" int ttb_dbg_tclk(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tclk, sizeof(unsigned long long) * 160 * 64) == cudaSuccess ? 0 : 5;
+}
+#define TTB_TSTAMP(idx)                                        \
+  do {                                                         \
+    unsigned long long tnow;                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));   \
+    g_tclk[blockIdx.x * 64 + (idx)] = tnow;                    \
+  } while (0)
+#else
+#define TTB_TSTAMP(idx) \
+  do {                  \
+  } while (0)
+#endif
+
+// Column-loop hooks of a tree node.
+//  inputs: complete (level 0: loaded whole at the start) or streamed: warp
+//    0 polls the children's progress counters one step ahead (the acquire
+//    load is issued at the start of a step and tested at its end) and, when
+//    a chunk of rows is final in every child, lane c bulk-copies child c's
+//    rows into the shared staging area (one mbarrier per chunk); the other
+//    warps wait on that barrier only when they reach the chunk.
+//  outputs: after step j every warp writes row j of R (its columns) into
+//    the node's row-major stream and, per finished chunk, bumps the node's
+//    progress counter.
 template <class C>
-__global__ void __launch_bounds__(C::NT, 1)
-tsqr_tree_kernel(const double* __restrict__ Rin, int n_in, int b, int f, double* __restrict__ Yn,
-                 double* __restrict__ Tn, double* __restrict__ Rout) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
-  const int q = blockIdx.x;
-  const int c0 = q * f, cnt = min(f, n_in - c0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int lc = lane / C::LR, lr = lane % C::LR;
-  double A[C::RPL][C::CPL];
-#pragma unroll
-  for (int s = 0; s < C::RPL; ++s) {
-    const int r = C::row(s, lr);
-    const int ch = r / b, rr = r - ch * b;
-#pragma unroll
-    for (int u = 0; u < C::CPL; ++u) {
-      const int k = col_of<C>(u, warp, lc);
-      A[s][u] = (ch < cnt && k < b) ? Rin[(int64_t)(c0 + ch) * b * b + rr + (int64_t)b * k] : 0.0;
+struct TreeHooks {
+  const double* Rin;        // complete inputs: children's triangles (col-major)
+  const double* Rrow_in;    // streamed inputs: children's row streams (ld ldr)
+  const unsigned* prog_in;  // streamed: children's counters (null: complete)
+  double* Rrow_out;         // this node's row stream (null: root)
+  unsigned* prog_out;
+  double* stage;            // shared: MC x ldr
+  unsigned long long* sbar; // shared: one per chunk
+  int c0, cnt, b, ldr, nchunks;
+  int next;                 // warp 0: next chunk to issue
+  unsigned pv;              // warp 0: pending progress value
+
+  __device__ __forceinline__ unsigned need(int ci) const { return (unsigned)C::NW * (unsigned)(ci + 1); }
+  __device__ __forceinline__ void issue(int ci) {
+    const int lane = threadIdx.x & 31;
+    const int j0 = ci * kTreeChunk, rows = min(kTreeChunk, b - j0);
+    const unsigned bytes = (unsigned)(rows * ldr * 8);
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    if (lane == 0) mbar_expect_tx(&sbar[ci], bytes * (unsigned)cnt);
+    __syncwarp();
+    for (int c = lane; c < cnt; c += 32)
+      bulk_g2s(stage + ((int64_t)c * b + j0) * ldr, Rrow_in + ((int64_t)(c0 + c) * b + j0) * ldr, bytes, &sbar[ci]);
+  }
+  // warp 0, blocking: issue every chunk that is already final (start-up)
+  __device__ __forceinline__ void poll_blocking(int upto) {
+    const int lane = threadIdx.x & 31;
+    while (next < nchunks && next <= upto) {
+      for (int c = lane; c < cnt; c += 32)
+        while (ld_acquire(prog_in + c) < need(next)) {
+        }
+      __syncwarp();
+      issue(next++);
     }
   }
+  __device__ __forceinline__ void pre(int) {
+    if (!prog_in || (threadIdx.x >> 5) != 0 || next >= nchunks) return;
+    const int lane = threadIdx.x & 31;
+    pv = 0xffffffffu;
+    for (int c = lane; c < cnt; c += 32) pv = min(pv, ld_relaxed(prog_in + c));
+  }
+  template <class T>
+  __device__ __forceinline__ void feed(T& A, int j0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lc = lane / C::LR, lr = lane % C::LR;
+    if (!prog_in) {  // complete inputs: everything at the start
+      if (j0 > 0) return;
+#pragma unroll
+      for (int s = 0; s < C::RPL; ++s) {
+        const int r = C::row(s, lr);
+        const int ch = r / b, i = r - ch * b;
+#pragma unroll
+        for (int t = 0; t < C::CPL; ++t) {
+          const int k = col_of<C>(t, warp, lc);
+          A[s][t] = (ch < cnt && k < b) ? Rin[(int64_t)(c0 + ch) * b * b + i + (int64_t)b * k] : 0.0;
+        }
+      }
+      return;
+    }
+    const int ci = j0 / kTreeChunk;
+    if (warp == 0) poll_blocking(ci);  // never blocks in steady state
+    mbar_wait(&sbar[ci], 0);
+    const int j1 = min(j0 + kTreeChunk, b);
+#pragma unroll
+    for (int s = 0; s < C::RPL; ++s) {
+      const int r = C::row(s, lr);
+      const int ch = r / b, i = r - ch * b;
+      if (ch >= cnt || i < j0 || i >= j1) continue;
+#pragma unroll
+      for (int t = 0; t < C::CPL; ++t) {
+        const int k = col_of<C>(t, warp, lc);
+        if (k < b) A[s][t] = k >= i ? stage[(int64_t)r * ldr + k] : 0.0;
+      }
+    }
+  }
+  template <class T>
+  __device__ __forceinline__ void post(T& A, int j) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef TTB_TCLK2
+    if (lane == 0 && warp == 0) TTB_TSTAMP(j);
+#endif
+    if (prog_in && warp == 0 && next < nchunks) {  // test the poll issued in pre()
+      const bool ok = __all_sync(0xffffffffu, pv >= need(next));
+      if (ok) {
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        issue(next++);
+      }
+    }
+    if (!prog_out) return;
+    const int lc = lane / C::LR, lr = lane % C::LR;
+    const int sj = 2 * (j / (2 * C::LR)) + (j & 1), lrj = (j % (2 * C::LR)) / 2;
+    if (lr == lrj) {
+#pragma unroll
+      for (int t = 0; t < C::CPL; ++t) {
+        const int k = col_of<C>(t, warp, lc);
+        if (k >= b) continue;
+        double v = 0.0;
+#pragma unroll
+        for (int s = 0; s < C::RPL; ++s)
+          if (s == sj) v = A[s][t];
+        Rrow_out[(int64_t)j * ldr + k] = k >= j ? v : 0.0;
+      }
+    }
+    if ((j + 1) % kTreeChunk == 0 || j + 1 == b) {
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");  // release this warp's rows
+      __syncwarp();
+      if (lane == 0) atomicAdd(prog_out, 1u);
+#if defined(TTB_TCLK) && !defined(TTB_TCLK_NOCHUNK)
+      if (lane == 0 && warp == 0) TTB_TSTAMP(j / kTreeChunk);
+#endif
+    }
+  }
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1) tsqr_tree_kernel(TreePlan tp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
+  unsigned long long* sbar = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(TileSmem<C>) + 127) & ~size_t(127)));
+  double* stage = reinterpret_cast<double*>(sbar + kMaxChunks);
+  const int node = blockIdx.x;
+  int L = 0;
+  while (L + 1 < tp.nlev && node >= tp.first[L + 1]) ++L;
+  const int q = node - tp.first[L];
+  const int b = tp.b, f = tp.f;
+  const int c0 = q * f, cnt = min(f, tp.n_in[L] - c0);
+  const int nchunks = (b + kTreeChunk - 1) / kTreeChunk;
+  double A[C::RPL][C::CPL];
+#pragma unroll
+  for (int s = 0; s < C::RPL; ++s)
+#pragma unroll
+    for (int t = 0; t < C::CPL; ++t) A[s][t] = 0.0;
   zero_G<C>(sm);
   init_ring<C>(sm);
+  if (threadIdx.x < nchunks) mbar_init(&sbar[threadIdx.x], 1);
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
-  tile_qr<C>(A, b, true, sm, 0);
-  store_Y<C>(A, b, true, Yn + (int64_t)q * C::MC * b, C::MC);
-  store_T<C>(sm, b, Tn + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
+#ifdef TTB_TCLK
+  if (threadIdx.x == 0) TTB_TSTAMP(63);
+#endif
+  const bool has_parent = L + 1 < tp.nlev;
+  TreeHooks<C> h;
+  h.Rin = tp.Rin[L];
+  h.Rrow_in = L > 0 ? tp.Rrow + (int64_t)tp.first[L - 1] * b * tp.ldr : nullptr;
+  h.prog_in = L > 0 ? tp.prog + tp.first[L - 1] + c0 : nullptr;
+  h.Rrow_out = has_parent ? tp.Rrow + (int64_t)node * b * tp.ldr : nullptr;
+  h.prog_out = has_parent ? tp.prog + node : nullptr;
+  h.stage = stage;
+  h.sbar = sbar;
+  h.c0 = c0;
+  h.cnt = cnt;
+  h.b = b;
+  h.ldr = tp.ldr;
+  h.nchunks = nchunks;
+  h.next = 0;
+  h.pv = 0;
+  tile_qr_t<C, true>(A, b, sm, 0, h);
+  store_Y<C>(A, b, true, tp.Y[L] + (int64_t)q * C::MC * b, C::MC);
+  store_T<C>(sm, b, tp.T[L] + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
   extract_R<C>(A, b, sm);
   __syncthreads();
+  double* Rout = tp.R[L] + (int64_t)q * b * b;
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
     const int r = idx % b, k = idx / b;
-    Rout[(int64_t)q * b * b + idx] = sm.Rs[r + C::BMAX * k];
+    Rout[idx] = sm.Rs[r + C::BMAX * k];
   }
 }
 
@@ -123,17 +337,6 @@ __global__ void sign_fix_kernel(const double* __restrict__ R, int b, double* __r
 // ------------------------------------------------------------------------
 constexpr int kApplyNT = 256;
 constexpr int kApplyKM = 64;   // max k
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // one thread: copy `bytes` (multiple of 16) from global to shared, signalling bar
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -378,6 +581,10 @@ namespace {
 
 template <class C>
 size_t tile_smem() { return sizeof(TileSmem<C>); }
+template <class C>
+size_t tree_smem() {
+  return ((sizeof(TileSmem<C>) + 127) & ~size_t(127)) + kMaxChunks * 8 + (size_t)C::MC * C::BMAX * 8;
+}
 
 template <class C>
 void set_smem_attr(const void* fn) {
@@ -399,32 +606,52 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   TTB_LAUNCHED();
   }
   auto tree = tsqr_tree_kernel<TC_>;
-  set_smem_attr<TC_>((const void*)tree);
-  const double* rin = f.Rleaf;
-  int n_in = f.plan.G;
-  for (int L = 0; L < f.nloc; ++L) {
-    int nodes = (n_in + f.ftree - 1) / f.ftree;
-    ProfScope ps("tsqr_tree", st);
-    tree<<<nodes, TC_::NT, tile_smem<TC_>(), st>>>(rin, n_in, f.b, f.ftree, f.locY[L], f.locT[L], f.locR[L]);
-    TTB_LAUNCHED();
-    rin = f.locR[L];
-    n_in = nodes;
+  {
+    static std::vector<const void*> done;
+    bool seen = false;
+    for (const void* p : done) seen |= (p == (const void*)tree);
+    if (!seen) {
+      TTB_CUDA(cudaFuncSetAttribute((const void*)tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem<TC_>()));
+      done.push_back((const void*)tree);
+    }
   }
-  f.Rlocal = (f.nloc > 0) ? f.locR[f.nloc - 1] : f.Rleaf;
+  // levels [0, n) of a tree over n_in complete inputs, one launch
+  auto run_tree = [&](const double* rin, int n_in, int nlev, double* const* Ys, double* const* Ts,
+                      double* const* Rs) {
+    TreePlan tp;
+    tp.nlev = nlev;
+    tp.b = f.b;
+    tp.f = f.ftree;
+    int total = 0;
+    for (int L = 0; L < nlev; ++L) {
+      const int nodes = (n_in + f.ftree - 1) / f.ftree;
+      tp.first[L] = total;
+      tp.n_in[L] = n_in;
+      tp.Rin[L] = rin;
+      tp.Y[L] = Ys[L];
+      tp.T[L] = Ts[L];
+      tp.R[L] = Rs[L];
+      total += nodes;
+      rin = Rs[L];
+      n_in = nodes;
+    }
+    tp.first[nlev] = total;
+    TTB_CHECK(total <= ctx.num_sms, TTB_ERR_CAPABILITY, "TSQR tree: more nodes than SMs");
+    tp.prog = f.prog;
+    tp.Rrow = f.Rrow;
+    tp.ldr = f.ldr;
+    TTB_CHECK((f.b + kTreeChunk - 1) / kTreeChunk <= kMaxChunks, TTB_ERR_CAPABILITY, "TSQR tree: too many chunks");
+    TTB_CUDA(cudaMemsetAsync(f.prog, 0, sizeof(unsigned) * total, st));
+    ProfScope ps("tsqr_tree", st);
+    tree<<<total, TC_::NT, tree_smem<TC_>(), st>>>(tp);
+    TTB_LAUNCHED();
+    return rin;
+  };
+  f.Rlocal = f.nloc > 0 ? run_tree(f.Rleaf, f.plan.G, f.nloc, f.locY, f.locT, f.locR) : f.Rleaf;
   if (ctx.nranks > 1) {
     // allgather the rank roots, then a redundant (bitwise identical) tree
     ctx.allgather(f.Rlocal, f.Rstack, (size_t)f.b * f.b);
-    rin = f.Rstack;
-    n_in = ctx.nranks;
-    for (int L = 0; L < f.nglob; ++L) {
-      int nodes = (n_in + f.ftree - 1) / f.ftree;
-      ProfScope ps("tsqr_tree", st);
-    tree<<<nodes, TC_::NT, tile_smem<TC_>(), st>>>(rin, n_in, f.b, f.ftree, f.gloY[L], f.gloT[L], f.gloR[L]);
-      TTB_LAUNCHED();
-      rin = f.gloR[L];
-      n_in = nodes;
-    }
-    f.Rraw = rin;
+    f.Rraw = f.nglob > 0 ? run_tree(f.Rstack, ctx.nranks, f.nglob, f.gloY, f.gloT, f.gloR) : f.Rstack;
   } else {
     f.Rraw = f.Rlocal;
   }
@@ -511,7 +738,9 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
     oGT[L] = add((int64_t)nodes_glo[L] * tsz);
     oGR[L] = add((int64_t)nodes_glo[L] * bb);
   }
-  size_t oD = add(b), oR = add(bb);
+  size_t oD = add(b), oR = add(bb), oP = add(ctx.num_sms);
+  f.ldr = (b + 1) & ~1;
+  size_t oRr = add((int64_t)ctx.num_sms * b * f.ldr);
   f.mem = ctx.alloc(total);
   char* base = (char*)f.mem;
   f.Y = (double*)(base + oY);
@@ -530,6 +759,8 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   }
   f.D = (double*)(base + oD);
   f.R = (double*)(base + oR);
+  f.prog = (unsigned*)(base + oP);
+  f.Rrow = (double*)(base + oRr);
   if (f.cls == 16) run_factor<Leaf16, Tree16>(ctx, f);
   else if (f.cls == 32) run_factor<Leaf32, Tree32>(ctx, f);
   else run_factor<Leaf64, Tree64>(ctx, f);

@@ -395,8 +395,27 @@ __device__ __forceinline__ void update_slot(double (&A)[C::RPL][C::CPL], const d
 // fulls barriers, the next producer on the empty barrier (slot reuse).
 // On exit: A holds the Householder vectors (head: R in the upper triangle
 // of rows < b, beta on the diagonal), sm.Gs holds T, sm.Rs holds R (body).
-template <class C, bool HEAD>
-__device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, int gbase) {
+// Hooks of the column loop (all no-ops for leaf tiles):
+//  h.feed(A, j0): called by every warp before any use of rows >= j0 (at the
+//    start and before each chunk of kTreeChunk columns): loads rows j0.. of
+//    late-arriving inputs into the register tile;
+//  h.pre(j) / h.post(A, j): start / end of column step j in every warp;
+//    post runs after the warp applied reflector j to all its columns, so
+//    row j of R is final in this warp's columns.
+struct NoHooks {
+  template <class T>
+  __device__ __forceinline__ void feed(T&, int) {}
+  __device__ __forceinline__ void pre(int) {}
+  template <class T>
+  __device__ __forceinline__ void post(T&, int) {}
+};
+#ifndef TTB_TREE_CHUNK
+#define TTB_TREE_CHUNK 4
+#endif
+constexpr int kTreeChunk = TTB_TREE_CHUNK;
+
+template <class C, bool HEAD, class H = NoHooks>
+__device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, int gbase, H&& h = H()) {
   constexpr int LR = C::LR, RPL = C::RPL, CPL = C::CPL, BM = C::BMAX;
   constexpr int T1 = CPL > 1 ? 1 : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -405,12 +424,15 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
 #pragma unroll
   for (int t = 0; t < CPL; ++t) kk[t] = col_of<C>(t, warp, lc);
 
+  h.feed(A, 0);
   if (warp == C::owner_warp(0)) {
     if (gbase >= kRing) mbar_wait(&sm.empty[gbase % kRing], ((gbase / kRing) - 1) & 1);
     publish<C, HEAD>(A, 0, gbase, sm);
   }
   for (int j = 0; j < b; ++j) {
     TTB_DCLK(0);
+    h.pre(j);
+    if ((j + 1) % kTreeChunk == 0 && j + 1 < b) h.feed(A, j + 1);  // before column j+1 is published
     const int gj = gbase + j;
     const int slot = gj % kRing;
     const int nx = j + 1;
@@ -480,6 +502,7 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
 #pragma unroll
     for (int t = 0; t < CPL; ++t)
       if (kk[t] < j && lr == 0) sm.Gs[kk[t] + BM * j] = d[t];
+    h.post(A, j);
   }
   __syncthreads();
   build_T<C>(sm, b);
