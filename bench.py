@@ -14,8 +14,10 @@ every core (the paper's 1 x P x 1 distribution) and the value is the whole
 tensor's algorithmic bytes over the max-over-ranks step time.
 
 value       = B_alg / t_step, B_alg = 8 (2|X| + |Y_out|)
-e2e         = same metric through the public API from pinned host buffers
-              (H2D of X, round_tt, D2H of the result inside the timed step)
+e2e         = same metric through the public host API (round_tt_host) from
+              page-locked host cores into page-locked output buffers: H2D of
+              X and D2H of the result inside every timed step, overlapped
+              with the sweeps by the library
 roofline    = dominant kernel class (TSQR leaf factorization), fp64-bound:
               reference Householder flops / its CUDA-event time, against the
               measured fp64 peak of this device (ttb_fp64_peak)
@@ -207,8 +209,13 @@ def run_ours(args):
     F = cost.rounding_flops(dims, rx, ry, "LRLI")
     value = B / (ms * 1e-3) / 1e9
 
-    # end-to-end through the public API from pinned host buffers
-    host_cores = [s.detach().cpu().pin_memory() for s in x.local]
+    # end-to-end through the public host API (round_tt_host: the drop-in for
+    # the reference's numpy-level call) from page-locked host cores into
+    # page-locked output buffers: every step uploads all input cores and
+    # downloads all output cores inside the timed region (the transfers
+    # overlap the sweeps inside the call)
+    host_cores = [s.detach().permute(2, 1, 0).contiguous().permute(2, 1, 0).cpu().pin_memory() for s in x.local]
+    host_out = [torch.empty(c.numel(), dtype=torch.float64).pin_memory() for c in host_cores]
     h2d = sum(c.numel() * 8 for c in host_cores)
     e2e_ms = []
     d2h = 0
@@ -218,19 +225,18 @@ def run_ours(args):
         a = torch.cuda.Event(enable_timing=True)
         bev = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        dev = [c.to(comm.device, non_blocking=True) for c in host_cores]
-        xt = T.DistTTTensor(comm, x.dims, x.ranks, dev)
-        o = T.round_tt(xt, opts)
-        res = [s.to("cpu", non_blocking=False) for s in o.local]
+        res, md = T.round_tt_host(host_cores, opts, comm=comm, out=host_out)
         bev.record(stream)
         torch.cuda.synchronize()
+        assert md["output_ranks"] == ry, md
         d2h = sum(r.numel() * 8 for r in res)
         if it >= args.warmup:
             e2e_ms.append(a.elapsed_time(bev))
-        del dev, xt, o, res
+        del res
     e2e_t = max_over_ranks(float(np.mean(e2e_ms)))
     e2e = {"value": B / (e2e_t * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_t,
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "api": "round_tt_host (ttb_round_host), page-locked host cores in and out"}
 
     # dominant-kernel roofline from one instrumented (event-timed) step
     dfma, dmma = _lib.fp64_peak(stream.cuda_stream)

@@ -112,6 +112,17 @@ int ttb_round(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim
               const int64_t* dims, const int64_t* ranks, const double* const* in,
               double* const* out, int64_t* out_ranks, double* meta);
 
+/* ttb_round on HOST-resident cores (the drop-in form of the reference's
+ * numpy-level call): in[n] / out[n] are host pointers (out[n] sized by the
+ * input ranks, results packed at the front as in ttb_round).  The upload of
+ * core n overlaps the orthonormalization sweep up to core n, and each
+ * output core is downloaded as soon as it is final.  Page-locked buffers
+ * (cudaHostAlloc / torch pin_memory) give full PCIe bandwidth; others are
+ * registered for the duration of the call.  Returns when out[] is filled. */
+int ttb_round_host(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim,
+                   const int64_t* dims, const int64_t* ranks, const double* const* in,
+                   double* const* out, int64_t* out_ranks, double* meta);
+
 /* ---- building blocks (the reference's lower-level public API) --------- */
 /* TSQR of the panel view of one slab (rl, I, rr): trans 0 -> V(X) (rows
  * r_left*I, cols rr), trans 1 -> H(X)^T (rows I*rr, cols rl).  A plain

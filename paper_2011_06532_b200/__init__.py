@@ -13,7 +13,8 @@ from .errors import (BoundsError, CapabilityError, CapacityError, ContractError,
                      NumericError, ShapeError, TTError)
 from .ops import add, add_n, hadamard, inner_product, norm, scale
 from .parallel import (ROUNDING_VARIANTS, RoundingOptions, TruncatedSVD, TSQRFactor, distribute, gather,
-                       orthonormalize, round_tt, serial_tt, truncated_svd, tsqr_apply_q, tsqr_factor)
+                       orthonormalize, round_tt, round_tt_host, serial_tt, truncated_svd, tsqr_apply_q,
+                       tsqr_factor)
 from .tensor import DistTTTensor, TTCore, TTTensor, block_bounds, random_tt
 
 __version__ = "0.1.0"
@@ -23,6 +24,6 @@ __all__ = [
     "DistComm", "DistTTTensor", "NumericError", "ROUNDING_VARIANTS", "RoundingOptions", "SerialComm",
     "ShapeError", "TSQRFactor", "TTCore", "TTError", "TTTensor", "TruncatedSVD", "add", "add_n",
     "block_bounds", "default_comm", "distribute", "gather", "hadamard", "inner_product", "norm",
-    "orthonormalize", "random_tt", "round_tt", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
+    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
     "tsqr_factor", "__version__",
 ]

@@ -97,6 +97,11 @@ cudaStream_t Ctx::side_stream() {
   return side;
 }
 
+cudaStream_t Ctx::copy_stream() {
+  if (!copy) TTB_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+  return copy;
+}
+
 }  // namespace ttb
 
 using namespace ttb;
@@ -141,6 +146,7 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
   if (ctx) {
     if (ctx->c.nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->c.nccl_comm);
     if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
+    if (ctx->c.copy) cudaStreamDestroy(ctx->c.copy);
     delete ctx;
   }
   TTB_TRY_END

@@ -22,6 +22,8 @@ struct Ctx {
   cudaStream_t side = nullptr;  // second stream for off-critical-path work (lazily created)
 
   cudaStream_t side_stream();
+  cudaStream_t copy = nullptr;  // host<->device transfers of the host API (lazily created)
+  cudaStream_t copy_stream();
   void* alloc(size_t bytes);
   void free(void* p);
   // collectives on this->stream (nranks > 1 only)

@@ -253,10 +253,80 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
   TTB_TRY_END
 }
 
-int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
-              const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks, double* meta) {
-  TTB_TRY_BEGIN
-  Ctx& ctx = h->c;
+// Host-resident cores for ttb_round_host: the H2D copy of every input core
+// is queued up front on the context's copy stream (one event per core) and
+// the compute stream waits for core n only where the sweep first reads it;
+// every output core is copied back as soon as it is final (event on the
+// stream that finished it), so both transfers overlap the sweeps.  Host
+// buffers that are not page-locked are registered for the duration of the
+// call (cudaHostRegister) so the copies stay asynchronous.
+struct HostIO {
+  Ctx& ctx;
+  int N;
+  const double* const* hin;
+  double* const* hout;
+  std::vector<cudaEvent_t> in_ev;
+  std::vector<char> waited;
+  std::vector<cudaEvent_t> evs;
+  std::vector<void*> registered;
+  HostIO(Ctx& c, int n, const double* const* in, double* const* out)
+      : ctx(c), N(n), hin(in), hout(out), in_ev(n, nullptr), waited(n, 0) {}
+  cudaStream_t cs() { return ctx.copy_stream(); }
+  void pin(const void* p, size_t bytes) {
+    if (!p || bytes == 0) return;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess && (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
+                                                          a.type == cudaMemoryTypeManaged))
+      return;
+    cudaGetLastError();
+    if (cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault) == cudaSuccess)
+      registered.push_back(const_cast<void*>(p));
+    else
+      cudaGetLastError();  // copies stay correct, just synchronous
+  }
+  void upload(int n, double* dst, int64_t count) {
+    pin(hin[n], (size_t)count * sizeof(double));
+    pin(hout[n], (size_t)count * sizeof(double));
+    TTB_CUDA(cudaMemcpyAsync(dst, hin[n], (size_t)count * sizeof(double), cudaMemcpyHostToDevice, cs()));
+    TTB_CUDA(cudaEventCreateWithFlags(&in_ev[n], cudaEventDisableTiming));
+    TTB_CUDA(cudaEventRecord(in_ev[n], cs()));
+  }
+  void need(int n, cudaStream_t st) {
+    if (n < 0 || n >= N || waited[n]) return;
+    TTB_CUDA(cudaStreamWaitEvent(st, in_ev[n], 0));
+    waited[n] = 1;
+  }
+  void ready(int n, const double* src, int64_t count, cudaStream_t st) {
+    cudaEvent_t e;
+    TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TTB_CUDA(cudaEventRecord(e, st));
+    TTB_CUDA(cudaStreamWaitEvent(cs(), e, 0));
+    evs.push_back(e);
+    TTB_CUDA(cudaMemcpyAsync(hout[n], src, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, cs()));
+  }
+  void finish() {
+    // the compute stream must not run past the copies (device buffers are
+    // freed stream-ordered on it), and the caller reads host memory
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(e, cs());
+      cudaStreamWaitEvent(ctx.stream, e, 0);
+      cudaEventDestroy(e);
+    }
+    cudaStreamSynchronize(cs());
+    for (auto e2 : in_ev)
+      if (e2) cudaEventDestroy(e2);
+    for (auto e2 : evs) cudaEventDestroy(e2);
+    for (void* p : registered) cudaHostUnregister(p);
+    in_ev.clear();
+    evs.clear();
+    registered.clear();
+  }
+};
+
+static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
+                       const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks,
+                       double* meta, HostIO* io) {
   check_chain(ndim, dims, ranks);
   TTB_CHECK(variant >= 0 && variant <= 3, TTB_ERR_CONTRACT, "unknown rounding variant");
   TTB_CHECK(eps0 >= 0.0, TTB_ERR_CONTRACT, "eps0 must be nonnegative");
@@ -270,9 +340,11 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
   meta[2] = 0.0;  // error_bound_violated
   meta[3] = 0.0;  // zero
   if (N == 1) {
+    if (io) io->need(0, ctx.stream);
     copy_d2d(ctx, out[0], in[0], r[0] * d[0] * r[1]);
     for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
-    return TTB_OK;
+    if (io) io->ready(0, out[0], r[0] * d[0] * r[1], ctx.stream);
+    return;
   }
   const int mr = max_rank > 0 ? (int)std::min<int64_t>(max_rank, 1 << 30) : 0;
   std::vector<Tsqr> facs(N);
@@ -287,7 +359,9 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
     for (int n = 0; n < N - 1; ++n) {
       const double* src = (n == 0) ? in[0] : out[n];
       const int b = (int)r[n + 1];
+      if (io && n == 0) io->need(0, ctx.stream);
       tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 0), facs[n]);
+      if (io) io->need(n + 1, ctx.stream);
       if (!implicit) {
         double* eye = make_eye(ctx, b);
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], r[n], d[n], b, 0));
@@ -302,7 +376,9 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
     for (int n = N - 1; n >= 1; --n) {
       const double* src = (n == N - 1) ? in[N - 1] : out[n];
       const int b = (int)r[n];
+      if (io && n == N - 1) io->need(N - 1, ctx.stream);
       tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 1), facs[n]);
+      if (io) io->need(n - 1, ctx.stream);
       if (!implicit) {
         double* eye = make_eye(ctx, b);
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], b, d[n], r[n + 1], 1));
@@ -326,7 +402,9 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
     for (int n = 0; n <= N; ++n) out_ranks[n] = 1;
     meta[3] = 1.0;
     if (scratch) ctx.free(scratch);
-    return TTB_OK;
+    if (io)
+      for (int n = 0; n < N; ++n) io->ready(n, out[n], d[n], ctx.stream);
+    return;
   }
   const double eps = eps0 * nx / std::sqrt((double)(N - 1));
   meta[1] = eps;
@@ -355,9 +433,11 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
         gemm_small_right(ctx, Mb, b, keep, out[n - 1], so.C, b, false, scratch);
         copy_d2d(ctx, out[n - 1], scratch, Mb * keep);
       }
+      if (io) io->ready(n, out[n], (int64_t)keep * d[n] * r[n + 1], sctx.stream);
       side_end(ctx, sctx, f2, so.mem);
       r[n] = keep;
     }
+    if (io) io->ready(0, out[0], r[0] * d[0] * r[1], ctx.stream);
   } else {
     for (int n = 0; n < N - 1; ++n) {
       const int b = (int)r[n + 1];
@@ -377,16 +457,71 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
         gemm_small_left(ctx, keep, b, Nb, so.C, b, true, out[n + 1], scratch);
         copy_d2d(ctx, out[n + 1], scratch, keep * Nb);
       }
+      if (io) io->ready(n, out[n], r[n] * d[n] * (int64_t)keep, sctx.stream);
       side_end(ctx, sctx, f2, so.mem);
       r[n + 1] = keep;
     }
+    if (io) io->ready(N - 1, out[N - 1], r[N - 1] * d[N - 1] * r[N], ctx.stream);
   }
   side_join(ctx, sctx);
   if (scratch) ctx.free(scratch);
   meta[2] = violated ? 1.0 : 0.0;
   for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
+}
+
+int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
+              const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks, double* meta) {
+  TTB_TRY_BEGIN
+  round_impl(h->c, variant, eps0, max_rank, ndim, dims, ranks, in, out, out_ranks, meta, nullptr);
   TTB_TRY_END
 }
+
+int ttb_round_host(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
+                   const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks,
+                   double* meta) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, ranks);
+  TTB_CHECK(in && out, TTB_ERR_CONTRACT, "null core pointer array");
+  std::vector<int64_t> sz(ndim);
+  int64_t total = 0;
+  for (int n = 0; n < ndim; ++n) {
+    sz[n] = ranks[n] * dims[n] * ranks[n + 1];
+    total += (sz[n] + 31) / 32 * 32;
+  }
+  // device images of the input and output cores (output cores sized by the
+  // input ranks, as ttb_round)
+  double* dmem = (double*)ctx.alloc((size_t)std::max<int64_t>(2 * total, 1) * sizeof(double));
+  std::vector<const double*> din(ndim);
+  std::vector<double*> dout(ndim);
+  int64_t off = 0;
+  for (int n = 0; n < ndim; ++n) {
+    din[n] = dmem + off;
+    dout[n] = dmem + total + off;
+    off += (sz[n] + 31) / 32 * 32;
+  }
+  HostIO io(ctx, ndim, in, out);
+  {  // the copy stream may only touch dmem after its stream-ordered allocation
+    cudaEvent_t e;
+    TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TTB_CUDA(cudaEventRecord(e, ctx.stream));
+    TTB_CUDA(cudaStreamWaitEvent(io.cs(), e, 0));
+    TTB_CUDA(cudaEventDestroy(e));
+  }
+  for (int n = 0; n < ndim; ++n) io.upload(n, const_cast<double*>(din[n]), sz[n]);
+  try {
+    round_impl(ctx, variant, eps0, max_rank, ndim, dims, ranks, din.data(), dout.data(), out_ranks, meta, &io);
+  } catch (...) {
+    io.finish();
+    ctx.free(dmem);
+    throw;
+  }
+  io.finish();
+  ctx.free(dmem);
+  TTB_TRY_END
+}
+
+
 
 int ttb_tsqr_factor(ttb_ctx* h, int64_t rl, int64_t I, int64_t rr, int trans, const double* slab, ttb_tsqr** out,
                     double* r_out) {

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from .comm import default_comm
 from .errors import ContractError, ShapeError
-from .tensor import (DistTTTensor, TTCore, TTTensor, block_bounds, f_empty, f_view,
+from .tensor import (DistTTTensor, TTCore, TTTensor, block_bounds, f_empty, f_view, is_f_slab,
                      to_host_array)
 
 ROUNDING_VARIANTS = ("LRLI", "LRL", "RLRI", "RLR")
@@ -207,6 +207,97 @@ def round_tt(dt: DistTTTensor, opts: RoundingOptions) -> DistTTTensor:
             md["eps_bond"] = float(meta[1])
             md["output_ranks"] = ranks
     return DistTTTensor(dt.comm, dt.dims, ranks, slabs, md)
+
+
+def _host_f_array(a):
+    """(array, data pointer) of an F-contiguous float64 host core: numpy
+    arrays and CPU torch tensors (pinned or not) pass without a copy when
+    they already have that layout."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if a.device.type != "cpu":
+            raise ContractError("round_tt_host takes host cores; use round_tt for device slabs")
+        t = a.to(torch.float64)
+        if t.dim() != 3:
+            raise ShapeError(f"core must be 3-way, got ndim={t.dim()}")
+        if not is_f_slab(t):
+            t = t.permute(2, 1, 0).contiguous().permute(2, 1, 0)
+        return t, t.data_ptr()
+    arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim != 3:
+        raise ShapeError(f"core must be 3-way, got ndim={arr.ndim}")
+    return arr, arr.ctypes.data
+
+
+def round_tt_host(cores, opts: RoundingOptions, comm=None, out=None):
+    """round_tt on host-resident cores -- the drop-in for the reference's
+    numpy-level ``round_tt(x)`` (parallel.py:293-438): this rank's cores
+    (F-order (r_left, I_local, r_right) numpy arrays or CPU tensors, or a
+    host TTTensor) go in, rounded host cores come out.  Uploads overlap the
+    orthonormalization sweep and each output core is downloaded as soon as
+    it is final (ttb_round_host).  ``out`` optionally supplies the output
+    buffers (flat host arrays / tensors of at least r_left*I*r_right input
+    entries each; page-locked ones avoid per-call registration).
+
+    Returns (cores, meta): F-order views into the output buffers, and the
+    reference's meta dict (norm, eps_bond, output_ranks, ...)."""
+    if isinstance(cores, TTTensor):
+        cores = [c.array for c in cores.cores]
+    comm = comm or default_comm()
+    arrs = [_host_f_array(c) for c in cores]
+    N = len(arrs)
+    if N == 0:
+        raise ShapeError("a TT tensor needs at least one core")
+    shapes = [tuple(int(x) for x in a.shape) for a, _ in arrs]
+    ranks = (shapes[0][0],) + tuple(sh[2] for sh in shapes)
+    for n in range(N - 1):
+        if shapes[n][2] != shapes[n + 1][0]:
+            raise ShapeError(f"rank mismatch between cores {n} and {n + 1}")
+    ldims = [sh[1] for sh in shapes]
+    if out is None:
+        out = [np.empty(max(1, sh[0] * sh[1] * sh[2]), dtype=np.float64) for sh in shapes]
+    if len(out) != N:
+        raise ShapeError("out must hold one buffer per core")
+    optr = []
+    for n, o in enumerate(out):
+        need = shapes[n][0] * shapes[n][1] * shapes[n][2]
+        if isinstance(o, np.ndarray):
+            if o.dtype != np.float64 or not o.flags.c_contiguous or o.size < need:
+                raise ShapeError(f"out[{n}] must be a contiguous float64 buffer of >= {need} entries")
+            optr.append(o.ctypes.data)
+        else:
+            if o.dtype.__str__() != "torch.float64" or not o.is_contiguous() or o.numel() < need or o.device.type != "cpu":
+                raise ShapeError(f"out[{n}] must be a contiguous float64 host tensor of >= {need} entries")
+            optr.append(o.data_ptr())
+    out_ranks = (C.c_int64 * (N + 1))()
+    meta = (C.c_double * 4)()
+    pin = (C.c_void_p * N)(*[p for _, p in arrs])
+    pout = (C.c_void_p * N)(*optr)
+    _lib.check(_lib.load().ttb_round_host(comm.ctx(), _VARIANT_CODE[opts.variant], float(opts.eps0),
+                                          int(opts.max_rank or 0), N, _lib.i64_array(ldims),
+                                          _lib.i64_array(ranks), pin, pout, out_ranks, meta))
+    rk = tuple(int(r) for r in out_ranks)
+    res = []
+    for n in range(N):
+        cnt = rk[n] * ldims[n] * rk[n + 1]
+        o = out[n]
+        if isinstance(o, np.ndarray):
+            res.append(o[:cnt].reshape((rk[n], ldims[n], rk[n + 1]), order="F"))
+        else:
+            res.append(f_view(o, rk[n], ldims[n], rk[n + 1]))
+    md = {"variant": opts.variant, "eps0": opts.eps0, "error_bound_violated": bool(meta[2])}
+    if N > 1:
+        md["norm"] = float(meta[0])
+        if meta[3]:
+            md["zero"] = True
+        else:
+            md["eps_bond"] = float(meta[1])
+            md["output_ranks"] = rk
+    del arrs  # keep the (possibly converted) inputs alive until here
+    return res, md
 
 
 # ----------------------------------------------------------------------------

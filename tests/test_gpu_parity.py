@@ -251,3 +251,44 @@ def test_round_eps_zero_bounds():
     ref, _ = O.round_tt(t, 0.0, "RLR")
     assert out.ranks == O.ranks_of(ref)
     assert O.rel_diff(host(out), t) < 1e-12
+
+
+@pytest.mark.parametrize("variant", ["LRLI", "LRL", "RLRI", "RLR"])
+def test_round_host_matches_device(variant):
+    """ttb_round_host (host cores in/out, streamed) runs the same kernels as
+    ttb_round: results are bitwise identical, against the golden too."""
+    g = golden()
+    x = tt("round_in")
+    for tag, eps in (("e2", 1e-2), ("e6", 1e-6)):
+        opts = T.RoundingOptions(eps, variant)
+        dev_out = T.round_tt(dev(x), opts)
+        cores, meta = T.round_tt_host(x, opts)  # pageable numpy in / out
+        assert meta["output_ranks"] == dev_out.ranks
+        bitwise(cores, host(dev_out))
+        assert O.rel_diff(cores, tt(f"round_{variant}_{tag}")) < TOL_TT
+        assert meta["norm"] == pytest.approx(float(g[f"round_{variant}_{tag}/norm"]), rel=TOL_SCALAR)
+
+
+def test_round_host_pinned_cfg1():
+    """Page-locked torch buffers in and out (the bench e2e path), cfg1 size."""
+    y = O.random_cores((2000,) * 8, (1,) + (10,) * 7 + (1,), 0)
+    x = O.add(y, y)
+    ref, meta_ref = O.round_tt(x, 1e-10, "LRLI")
+    hin = [torch.from_numpy(np.asfortranarray(c)).permute(2, 1, 0).contiguous().permute(2, 1, 0).pin_memory()
+           for c in x]
+    outs = [torch.empty(c.size, dtype=torch.float64).pin_memory() for c in x]
+    cores, meta = T.round_tt_host(hin, T.RoundingOptions(1e-10), out=outs)
+    assert meta["output_ranks"] == O.ranks_of(ref)
+    got = [np.asfortranarray(c.numpy()) for c in cores]
+    assert O.rel_diff(got, ref) < TOL_TT
+    assert meta["norm"] == pytest.approx(meta_ref["norm"], rel=TOL_SCALAR)
+
+
+def test_round_host_zero_and_single_mode():
+    x = [np.zeros_like(c) for c in O.random_cores((4, 5, 4), (1, 3, 3, 1), 2)]
+    cores, meta = T.round_tt_host(x, T.RoundingOptions(1e-6, "RLR"))
+    assert meta.get("zero") is True and [c.shape for c in cores] == [(1, 4, 1), (1, 5, 1), (1, 4, 1)]
+    assert not any(np.any(c) for c in cores)
+    s = O.random_cores((7,), (1, 1), 5)
+    cores, _ = T.round_tt_host(s, T.RoundingOptions(1e-6, "RLR"))
+    bitwise(cores, s)
