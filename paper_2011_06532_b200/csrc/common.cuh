@@ -41,7 +41,8 @@ void count_launch(int n = 1);
   do {                                                                            \
     cudaError_t _e = cudaGetLastError();                                          \
     if (_e != cudaSuccess)                                                        \
-      TTB_THROW(TTB_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(_e)); \
+      TTB_THROW(TTB_ERR_CUDA, std::string("kernel launch failed (") + __FILE__ + ":" + std::to_string(__LINE__) + \
+                                  "): " + cudaGetErrorString(_e));                                      \
     ::ttb::count_launch();                                                        \
   } while (0)
 

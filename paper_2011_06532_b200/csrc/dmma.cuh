@@ -32,6 +32,7 @@ __device__ __forceinline__ void cta_dmma(int M, int N, int K, int nwarps, AF a, 
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
     for (int k0 = 0; k0 < K; k0 += 4) {
       const double a0 = a(m0 + fr, k0 + fc), a1 = a(m0 + 8 + fr, k0 + fc);
       const double b0 = b(k0 + fc, n0 + fr), b1 = b(k0 + fc, n0 + 8 + fr);

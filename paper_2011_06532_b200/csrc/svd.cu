@@ -20,10 +20,11 @@
 
 namespace ttb {
 
-constexpr int kSvdNT = 256;
+constexpr int kSvdNT = 512;  // 256 threads on the A columns, 256 trailing on V
 constexpr int kSvdMax = 64;
 constexpr int kLd = kSvdMax + 1;  // padded column stride: distinct columns start on distinct banks
 constexpr int kGrp = 8;  // threads per column pair
+constexpr int kHalf = kSvdNT / 2;
 
 #ifdef TTB_DEBUG_CLK
 static __device__ long long g_sclk[64 * 4];
@@ -35,22 +36,50 @@ static __device__ long long g_sclk[64 * 4];
 struct SvdSmem {
   double A[kLd * kSvdMax];   // ld = kLd
   double V[kLd * kSvdMax];
+  double nrm[kSvdMax];           // squared column norms, updated with each rotation
+  double rot[2][kSvdMax / 2][2]; // (cs, sn) of each pair of a round (0, 0: none), by round parity
   double sig[kSvdMax];
   int order[kSvdMax];
-  int slot[kSvdMax];             // tournament position -> column
   int rotated;
   int bad;
 };
 
-// reduction over the 8 lanes of one pair group; the mask names only those
-// lanes because neighbouring groups of the warp may be idle (padding pair)
+// reduction over the 8 lanes of one pair group (every lane of the warp
+// takes part: each group owns exactly one pair slot, padding slots reduce
+// zeros, so the full mask is uniform and the shuffles never serialize)
 __device__ __forceinline__ double grp_sum(double v) {
-  const unsigned mask = 0xFFu << ((threadIdx.x & 31) & ~(kGrp - 1));
 #pragma unroll
-  for (int off = kGrp / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
+  for (int off = kGrp / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
 }
 
+// columns (p, q) of pair pr in round `round` of the circle-method tournament
+// (pr < np/2, round < np-1; no integer division)
+__device__ __forceinline__ void pair_of(int pr, int round, int np, int& p, int& q) {
+  const int M1 = np - 1;
+  if (pr == 0) {
+    p = M1;
+    q = round;
+  } else {
+    p = round + pr;
+    p -= p >= M1 ? M1 : 0;
+    q = round - pr;
+    q += q < 0 ? M1 : 0;
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+// Threads [0, kHalf) run the rotations on A (the serial chain of the
+// algorithm); threads [kHalf, kSvdNT) apply each round's rotations to V one
+// round later, off that chain.  Column norms are carried along (updated by
+// each rotation, recomputed exactly at every sweep start), so a pair needs
+// one dot product, not three.  Pairs whose columns are both at roundoff
+// level of the largest column are left alone: rotating them cannot change
+// the result above roundoff.
 __global__ void __launch_bounds__(kSvdNT, 1)
 jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int transA, double eps,
                   int max_rank, double* __restrict__ C, double* __restrict__ Vk, double* __restrict__ s_out,
@@ -69,74 +98,107 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     sm.A[r + kLd * c] = v;
     sm.V[r + kLd * c] = (r == c && c < n) ? 1.0 : 0.0;
   }
-  for (int c = tid; c < np; c += kSvdNT) sm.slot[c] = c;
   __syncthreads();
 
-  const int grp = tid / kGrp, gl = tid % kGrp;
+  const bool vside = tid >= kHalf;
+  const int ltid = vside ? tid - kHalf : tid;
+  const int grp = ltid / kGrp, gl = ltid % kGrp;
   const int npairs = np / 2;
   const double tol = 4.0 * 2.220446049250313e-16 * sqrt((double)m);
   const double tol2 = tol * tol;
+  const double noise2 = 2.220446049250313e-16 * 2.220446049250313e-16;
   int sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
+    // exact squared column norms (one warp per column, A side)
+    if (!vside) {
+      for (int c = ltid / 32; c < np; c += kHalf / 32) {
+        double acc = 0.0;
+        for (int r = ltid % 32; r < m; r += 32) acc = fma(sm.A[r + kLd * c], sm.A[r + kLd * c], acc);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if ((ltid % 32) == 0) sm.nrm[c] = acc;
+      }
+    }
     if (tid == 0) sm.rotated = 0;
     __syncthreads();
-    for (int round = 0; round < np - 1; ++round) {
-      // pair grp: slots (grp, np-1-grp) of the current tournament table
+    double nmax = 0.0;
+    for (int c = 0; c < n; ++c) nmax = fmax(nmax, sm.nrm[c]);
+    const double floor2 = noise2 * nmax;
+    for (int round = 0; round <= np - 1; ++round) {
       SVD_CLK(0);
-      for (int pr = grp; pr < npairs; pr += kSvdNT / kGrp) {
-        // circle-method round robin: player np-1 fixed, the rest rotate
-        const int M1 = np - 1;
-        int p = pr == 0 ? M1 : (round + pr) % M1;
-        int q = pr == 0 ? round : (round - pr + M1) % M1;
-        if (p > q) { int t = p; p = q; q = t; }
-        if (q < n) {
+      if (!vside) {
+        if (round < np - 1) {
+          // one pair slot per group (npairs <= kHalf / kGrp): the whole
+          // warp reaches the shuffles together
+          const int pr = grp;
+          int p = 0, q = 0;
+          const bool live = pr < npairs;
+          if (live) pair_of(pr, round, np, p, q);
+          const bool valid = live && q < n;
           double* ap = sm.A + kLd * p;
           double* aq = sm.A + kLd * q;
-          // rows gl, gl+8, ...: fixed trip count (rows >= m are zero), loads batched
           double xa[kSvdMax / kGrp], ya[kSvdMax / kGrp];
 #pragma unroll
           for (int u = 0; u < kSvdMax / kGrp; ++u) {
-            xa[u] = ap[gl + kGrp * u];
-            ya[u] = aq[gl + kGrp * u];
+            xa[u] = valid ? ap[gl + kGrp * u] : 0.0;
+            ya[u] = valid ? aq[gl + kGrp * u] : 0.0;
           }
-          double al = 0.0, be = 0.0, ga = 0.0;
+          double g0 = 0.0, g1 = 0.0;
 #pragma unroll
-          for (int u = 0; u < kSvdMax / kGrp; ++u) {
-            al = fma(xa[u], xa[u], al);
-            be = fma(ya[u], ya[u], be);
-            ga = fma(xa[u], ya[u], ga);
+          for (int u = 0; u < kSvdMax / kGrp; u += 2) {
+            g0 = fma(xa[u], ya[u], g0);
+            g1 = fma(xa[u + 1], ya[u + 1], g1);
           }
+          const double al = valid ? sm.nrm[p] : 0.0, be = valid ? sm.nrm[q] : 0.0;
           SVD_CLK(1);
-          al = grp_sum(al);
-          be = grp_sum(be);
-          ga = grp_sum(ga);
+          const double ga = grp_sum(g0 + g1);
           SVD_CLK(2);
-          if (ga != 0.0 && ga * ga > tol2 * al * be) {
-            // Rutishauser: zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            const double cs = rsqrt(fma(t, t, 1.0));
-            const double sn = cs * t;
+          double cs = 0.0, sn = 0.0;
+          if (valid && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > floor2) {
+            // Rutishauser, division-light: t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+            // zeta = (be - al) / (2 ga)  ->  t = s 2|ga| / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
+            const double dif = be - al;
+            const double den = fabs(dif) + sqrt(fma(dif, dif, 4.0 * ga * ga));
+            const double tabs = 2.0 * fabs(ga) * __drcp_rn(den);
+            const double t = ((dif >= 0.0) == (ga >= 0.0)) ? tabs : -tabs;
+            cs = rsqrt(fma(t, t, 1.0));
+            sn = cs * t;
             SVD_CLK(3);
 #pragma unroll
             for (int u = 0; u < kSvdMax / kGrp; ++u) {
               ap[gl + kGrp * u] = cs * xa[u] - sn * ya[u];
               aq[gl + kGrp * u] = sn * xa[u] + cs * ya[u];
             }
-            double* vp = sm.V + kLd * p;
-            double* vq = sm.V + kLd * q;
-            double xv[kSvdMax / kGrp], yv[kSvdMax / kGrp];
-#pragma unroll
-            for (int u = 0; u < kSvdMax / kGrp; ++u) {
-              xv[u] = vp[gl + kGrp * u];
-              yv[u] = vq[gl + kGrp * u];
+            if (gl == 0) {
+              sm.nrm[p] = fma(-t, ga, al);
+              sm.nrm[q] = fma(t, ga, be);
+              sm.rotated = 1;
             }
+          }
+          if (live && gl == 0) {
+            sm.rot[round & 1][pr][0] = cs;
+            sm.rot[round & 1][pr][1] = sn;
+          }
+        }
+      } else if (round > 0) {  // V side: the previous round's rotations
+        const int rr = round - 1;
+        for (int pr = grp; pr < npairs; pr += kHalf / kGrp) {
+          const double cs = sm.rot[rr & 1][pr][0], sn = sm.rot[rr & 1][pr][1];
+          if (cs == 0.0) continue;
+          int p, q;
+          pair_of(pr, rr, np, p, q);
+          double* vp = sm.V + kLd * p;
+          double* vq = sm.V + kLd * q;
+          double xv[kSvdMax / kGrp], yv[kSvdMax / kGrp];
 #pragma unroll
-            for (int u = 0; u < kSvdMax / kGrp; ++u) {
-              vp[gl + kGrp * u] = cs * xv[u] - sn * yv[u];
-              vq[gl + kGrp * u] = sn * xv[u] + cs * yv[u];
-            }
-            if (gl == 0) sm.rotated = 1;
+          for (int u = 0; u < kSvdMax / kGrp; ++u) {
+            xv[u] = vp[gl + kGrp * u];
+            yv[u] = vq[gl + kGrp * u];
+          }
+#pragma unroll
+          for (int u = 0; u < kSvdMax / kGrp; ++u) {
+            vp[gl + kGrp * u] = cs * xv[u] - sn * yv[u];
+            vq[gl + kGrp * u] = sn * xv[u] + cs * yv[u];
           }
         }
       }
@@ -222,6 +284,7 @@ void jacobi_svd(Ctx& ctx, const double* A, int lda, int m, int n, bool transA, d
     attr = true;
   }
   ProfScope ps("jacobi_svd", ctx.stream);
+  static_assert(kSvdMax / 2 <= kHalf / kGrp, "one pair slot per thread group");
   jacobi_svd_kernel<<<1, kSvdNT, sizeof(SvdSmem), ctx.stream>>>(A, lda, m, n, transA ? 1 : 0, eps, max_rank, C, Vk,
                                                                s, info, dinfo);
   TTB_LAUNCHED();

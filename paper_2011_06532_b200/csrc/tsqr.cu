@@ -426,7 +426,7 @@ struct ChainArgs {
   const double* zin;     // per CTA b x k (ld b)
   const double* D;       // sign fix when there is no tree above (else null)
   int k;
-  double* u;             // per tile b x KP, row-major (l*KP + c); columns >= k unused
+  double* u;             // per tile b x ldpad(k), row-major (l*ldu + c); columns >= k unused
   double* z0;            // per CTA b x k: the head tile's input z_0
 };
 
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
   constexpr int NW = kApplyNT / 32;
   const int g = blockIdx.x;
   const LeafPlan& pl = a.plan;
-  const int b = pl.b, k = a.k, KP = kpad(k), ld = ldpad(b);
+  const int b = pl.b, k = a.k, KP = ldpad(k), ld = ldpad(b);  // KP: row stride of u
   const int64_t tsz = tstride_of(b);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // T double buffer
   double* const Zb0 = reinterpret_cast<double*>(smem_raw + 64);
@@ -510,6 +510,7 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
 struct ProductArgs {
   LeafPlan plan;
   int ldy;
+  int unit_rows;
   const double* Y;
   const double* u;
   const double* z0;
@@ -519,18 +520,23 @@ struct ProductArgs {
 
 // One CTA per tile: out_t = -Y_t u_t (+ z_0 on the head tile's top rows).
 // Y_t is bulk-copied column by column into a bank-padded shared layout.
-__global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int NW = kApplyNT / 32;
-  const LeafPlan& pl = a.plan;
-  const int b = pl.b, k = a.k, KP = kpad(k), ldy = a.ldy, rs = pl.rs, ni = pl.ni;
-  const int lys = ldpad(ldy), ldu = ldpad(k);
-  const int64_t tile = blockIdx.x;
-  // tile -> (CTA g, position t) of the factor's chains
+// Persistent: one CTA per SM walks work units blockIdx.x, +gridDim.x, ...
+// (a unit = 128 rows of one tile) with a two-stage bulk-copy pipeline: unit
+// i+1's rows of Y_t and its u_t stream into shared memory while unit i is
+// multiplied.
+constexpr int kProdStages = 2;
+constexpr int kProdRows = 128;  // unit rows when a whole tile does not fit two stages
+
+struct ProductUnit {
+  int rows;  // rows per work unit: the tile (ldy) or kProdRows
+  __host__ __device__ static size_t smem(int ur, int b, int k) {
+    return 128 + (size_t)kProdStages * ((size_t)(ur + 4) * b + (size_t)b * ldpad(k)) * sizeof(double);
+  }
+};
+
+__device__ __forceinline__ void product_tile_of(const LeafPlan& pl, int64_t tile, int& g, int64_t& t) {
   const int rem = pl.rem();
   const int64_t t1 = pl.tiles_of(pl.base() + 1), t0 = pl.tiles_of(pl.base());
-  int g;
-  int64_t t;
   if (tile < (int64_t)rem * t1) {
     g = (int)(tile / t1);
     t = tile - (int64_t)g * t1;
@@ -539,40 +545,77 @@ __global__ void __launch_bounds__(kApplyNT, 2) tsqr_product_kernel(ProductArgs a
     g = rem + (int)(x / t0);
     t = x - (int64_t)(g - rem) * t0;
   }
+}
+
+constexpr int kProdNT = 512;  // 16 warps: one 16x16 output block each per unit at k <= 32
+
+__global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NW = kProdNT / 32;
+  const LeafPlan& pl = a.plan;
+  const int b = pl.b, k = a.k, ldy = a.ldy, rs = pl.rs, ni = pl.ni;
+  const int UR = a.unit_rows;
+  const int lys = UR + 4;  // = ldpad(UR) for UR a multiple of 16
+  const int ldu = ldpad(k);
+  const int halves = ldy / UR;
+  const int64_t nunits = pl.total_tiles() * halves;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
-  double* Ys = reinterpret_cast<double*>(smem_raw + 64);
-  double* Us = Ys + (int64_t)lys * b;
-  const double* Yg = a.Y + tile * (int64_t)ldy * b;
+  double* Ysb = reinterpret_cast<double*>(smem_raw + 128);
+  const int64_t ystage = (int64_t)lys * b, ustage = (int64_t)b * ldu;
+  double* Usb = Ysb + kProdStages * ystage;
+  const unsigned ubytes = (unsigned)(ustage * 8);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    for (int s2 = 0; s2 < kProdStages; ++s2) mbar_init(&bar[s2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    mbar_expect_tx(bar, (unsigned)(ldy * b * 8));
   }
   __syncthreads();
-  if (threadIdx.x < 32)
-    for (int j = threadIdx.x; j < b; j += 32) bulk_g2s(Ys + lys * j, Yg + (int64_t)ldy * j, ldy * 8, bar);
-  const double* ug = a.u + tile * (int64_t)b * KP;
-  for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int l = idx / k, c = idx % k;
-    Us[l * ldu + c] = ug[l * KP + c];
+  // warp 0 issues the copies of one unit into a stage
+  auto issue = [&](int64_t unit, int st) {
+    if (threadIdx.x >= 32) return;
+    const int64_t tile = unit / halves;
+    const int r0 = (int)(unit - tile * halves) * UR;
+    if (threadIdx.x == 0) mbar_expect_tx(&bar[st], (unsigned)(UR * b * 8) + ubytes);
+    __syncwarp();
+    const double* Yg = a.Y + tile * (int64_t)ldy * b + r0;
+    for (int j = threadIdx.x; j < b; j += 32)
+      bulk_g2s(Ysb + st * ystage + (int64_t)lys * j, Yg + (int64_t)ldy * j, UR * 8, &bar[st]);
+    if (threadIdx.x == 0) bulk_g2s(Usb + st * ustage, a.u + tile * ustage, ubytes, &bar[st]);
+  };
+  int64_t unit = blockIdx.x;
+  if (unit < nunits) issue(unit, 0);
+  for (int it = 0; unit < nunits; ++it, unit += gridDim.x) {
+    const int st = it & 1;
+    const int64_t nxt = unit + gridDim.x;
+    if (nxt < nunits) {  // stage st^1 was released by the barrier that ended the previous unit
+      if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(nxt, st ^ 1);
+    }
+    const int64_t tile = unit / halves;
+    const int r0 = (int)(unit - tile * halves) * UR;
+    int g;
+    int64_t t;
+    product_tile_of(pl, tile, g, t);
+    const int64_t n_g = pl.count(g);
+    const int64_t ia = pl.start(g) + t * ni;
+    const int nsl = (int)min64(ni, n_g - t * ni);
+    const int rows = min(nsl * rs - r0, UR);
+    const bool head = (t == 0) && r0 == 0;
+    const double* z0 = a.z0 + (int64_t)g * b * k;
+    const double* Ys = Ysb + st * ystage;
+    const double* Us = Usb + st * ustage;
+    mbar_wait(&bar[st], (it >> 1) & 1);
+    if (rows > 0)
+      cta_dmma(
+          rows, k, b, NW, [&](int m, int l) { return (m < rows && l < b) ? Ys[m + lys * l] : 0.0; },
+          [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
+          [&](int m, int n, double v) {
+            const double base = (head && m < b) ? z0[m + b * n] : 0.0;
+            int si, w;
+            tile_row(a.out.trans, r0 + m, nsl, rs, si, w);
+            a.out.base[a.out.addr(w, ia + si, n)] = base - v;
+          });
+    __syncthreads();
   }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  const int64_t n_g = pl.count(g);
-  const int64_t ia = pl.start(g) + t * ni;
-  const int nsl = (int)min64(ni, n_g - t * ni);
-  const int rows = nsl * rs;
-  const bool head = (t == 0);
-  const double* z0 = a.z0 + (int64_t)g * b * k;
-  cta_dmma(
-      rows, k, b, NW, [&](int m, int l) { return (m < rows && l < b) ? Ys[m + lys * l] : 0.0; },
-      [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
-      [&](int m, int n, double v) {
-        const double base = (head && m < b) ? z0[m + b * n] : 0.0;
-        int si, w;
-        tile_row(a.out.trans, m, nsl, rs, si, w);
-        a.out.base[a.out.addr(w, ia + si, n)] = base - v;
-      });
 }
 // ------------------------------------------------------------------------
 // host side
@@ -779,16 +822,16 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   int64_t maxlev = 1;
   for (int L = 0; L < f.nloc; ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)lnodes[L] * f.ftree);
   for (size_t L = 0; L < gnodes.size(); ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)gnodes[L] * f.ftree);
-  const int64_t nscr = 2 * maxlev * bk + ntiles * b * KP + (int64_t)G * bk;
+  const int64_t nscr = 2 * maxlev * bk + ntiles * b * ldpad(k) + (int64_t)G * bk;
   double* scr = (double*)ctx.alloc((size_t)nscr * sizeof(double));
   double* lev[2] = {scr, scr + maxlev * bk};
   double* ubuf = scr + 2 * maxlev * bk;
-  double* z0buf = ubuf + ntiles * b * KP;
+  double* z0buf = ubuf + ntiles * b * ldpad(k);
   static bool attr = false;
   if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_tree_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_tree_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   const double* cur = z;
@@ -841,9 +884,13 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.z0 = z0buf;
   pa.k = k;
   pa.out = out;
-  const size_t psmem = 64 + (size_t)((int64_t)ldpad(f.ldy) * b + (int64_t)b * ldpad(k)) * sizeof(double);
+  TTB_CHECK(f.ldy % kProdRows == 0, TTB_ERR_CAPABILITY, "TSQR apply: tile rows not a multiple of 128");
+  pa.unit_rows = ProductUnit::smem(f.ldy, b, k) <= 200 * 1024 ? f.ldy : kProdRows;
+  const size_t psmem = ProductUnit::smem(pa.unit_rows, b, k);
   ProfScope ps("apply_product", ctx.stream);
-  tsqr_product_kernel<<<(unsigned)ntiles, kApplyNT, psmem, ctx.stream>>>(pa);
+  const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);
+  const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunits, ctx.num_sms));
+  tsqr_product_kernel<<<pgrid, kProdNT, psmem, ctx.stream>>>(pa);
   TTB_LAUNCHED();
   ctx.free(scr);
 }
