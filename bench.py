@@ -147,6 +147,22 @@ def make_input(T, comm, cfg, seed=0):
     return y, T.add(y, y)
 
 
+def leaf_traffic():
+    """DRAM bytes (read + write) of one leaf launch from the committed ncu
+    --set full capture (profiles/*_leaf_ncu.json, newest round), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_leaf_ncu.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        return {"bytes_per_launch": (d["dram_read_MB"] + d["dram_write_MB"]) * 1e6,
+                "algorithmic_bytes_per_launch": d["algorithmic_MB"] * 1e6,
+                "launch": d["launch"], "source": os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))}
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -254,7 +270,7 @@ def run_ours(args):
     peak_hbm, peak_src = hbm_peak()
     roofline = {"bound": "fp64", "kernel": "tsqr_leaf (Householder TSQR leaf chains)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": None, "peak_source": "measured fp64 (ttb_fp64_peak: DFMA %.1f, DMMA %.1f TF/s)" % (dfma, dmma),
+                "traffic": leaf_traffic(), "peak_source": "measured fp64 (ttb_fp64_peak: DFMA %.1f, DMMA %.1f TF/s)" % (dfma, dmma),
                 "launches": leaf_launch, "ms_per_step": leaf_ms,
                 "share_of_step": leaf_ms / ms if ms else None}
     step_roofline = {"hbm_frac": value / peak_hbm, "hbm_peak_gbs": peak_hbm, "hbm_peak_source": peak_src,
