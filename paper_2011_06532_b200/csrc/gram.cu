@@ -133,6 +133,200 @@ __global__ void __launch_bounds__(kGrNT, 2) gram_kernel(GramArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp64-MMA version with an S-stage bulk-copy pipeline (even ranks).
+//
+// For every right index the (left, slice) block of a chunk of NS slices is
+// contiguous in the F-order core, so a chunk of X and Y arrives as
+// rar + rbr bulk copies (TMA engine, mbarrier completion), S - 1 chunks
+// ahead.  Each warp owns one 8-wide tile of right indices b of X and a
+// share of the chunk's slices; per slice ii it computes
+//   Z^T(b, c) = sum_a X(a, ii, b) W(c, a)       (m8n8k4: A = X^T, B = W^T)
+// and feeds the D fragments of Z^T straight back as B fragments of
+//   acc(d, b) += sum_c Y(c, ii, d) Z(c, ii, b)
+// (a D fragment holds k = c = 2 fc + h for n = b = fr, i.e. two k4 steps
+// with the k order {0,2,4,6}, {1,3,5,7}; the A fragments of Y are loaded in
+// the same order, one 16-byte load for both steps).  Z never leaves the
+// registers, and the CTA synchronises once per chunk.  Leading dimensions:
+// X 4 mod 16, Y 8 mod 16, W 4 mod 16 (conflict-free fragment loads).
+// ---------------------------------------------------------------------------
+
+struct Gram2Args {
+  const double* W;  // rbl x ral (col-major)
+  const double* X;  // (ral, I, rar)
+  const double* Y;  // (rbl, I, rbr)
+  int ral, rar, rbl, rbr;
+  int64_t I;
+  int lns;          // log2(slices per chunk)
+  int stages;       // chunk buffers
+  int64_t per_cta;  // slices per CTA (multiple of the chunk)
+  int ldw, ldx, ldy;
+  double* part;     // gridDim.x partials of rbr x rar
+};
+
+__host__ __device__ __forceinline__ int g2_ld4(int n) { return ((n + 11) & ~15) + 4; }  // >= n, 4 mod 16
+__host__ __device__ __forceinline__ int g2_ld8(int n) { return ((n + 7) & ~15) + 8; }   // >= n, 8 mod 16
+
+__device__ __forceinline__ unsigned g2_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void g2_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   g2_smem(dst)),
+               "l"(src), "r"(bytes), "r"(g2_smem(bar))
+               : "memory");
+}
+__device__ __forceinline__ void g2_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(g2_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void g2_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(g2_smem(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void dmma884g(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// MAXD: d tiles of 8 this instantiation handles (rbr <= 8 MAXD); NT threads
+template <int MAXD, int NT>
+__global__ void __launch_bounds__(NT, 1) gram2_kernel(Gram2Args a) {
+  constexpr int kG2NT = NT, kG2NW = NT / 32, kG2MaxD = MAXD;
+  extern __shared__ __align__(128) double g2[];
+  const int ral = a.ral, rar = a.rar, rbl = a.rbl, rbr = a.rbr;
+  const int lns = a.lns, NS = 1 << lns, S = a.stages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int64_t xstage = (int64_t)rar * a.ldx, ystage = (int64_t)rbr * a.ldy;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(g2);  // S <= 16 barriers
+  double* Ws = g2 + 16;                            // Ws[c + ldw a]
+  double* Xs = Ws + (int64_t)a.ldw * ral;          // S stages: Xs[b * ldx + a + ral * ii]
+  Xs += (16 - ((Xs - g2) & 15)) & 15;              // 128-byte aligned stages
+  double* Ys = Xs + S * xstage;                    // S stages: Ys[d * ldy + c + rbl * ii]
+  if (tid < S) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g2_smem(&bar[tid])) : "memory");
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  for (int e = tid; e < rbl * ral; e += kG2NT) Ws[(e % rbl) + a.ldw * (e / rbl)] = a.W[e];
+
+  const int64_t s_begin = (int64_t)blockIdx.x * a.per_cta;
+  const int64_t s_end = min64(a.I, s_begin + a.per_cta);
+  const int nch = s_end > s_begin ? (int)((s_end - s_begin + NS - 1) >> lns) : 0;
+  __syncthreads();
+
+  auto issue = [&](int c, int st) {  // warp 0: one bulk copy per right index
+    if (warp != 0) return;
+    const int64_t i0 = s_begin + ((int64_t)c << lns);
+    const int nn = (int)min64(NS, s_end - i0);
+    const unsigned bx = (unsigned)(ral * nn * 8), by = (unsigned)(rbl * nn * 8);
+    if (lane == 0) g2_expect(&bar[st], bx * rar + by * rbr);
+    __syncwarp();
+    for (int b = lane; b < rar; b += 32)
+      g2_bulk(Xs + st * xstage + (int64_t)b * a.ldx, a.X + ral * (i0 + a.I * b), bx, &bar[st]);
+    for (int d = lane; d < rbr; d += 32)
+      g2_bulk(Ys + st * ystage + (int64_t)d * a.ldy, a.Y + rbl * (i0 + a.I * d), by, &bar[st]);
+  };
+
+  // warp -> (b tile, slice share)
+  const int nbt = (rar + 7) / 8;
+  const int wpb = kG2NW / nbt;              // warps per b tile (>= 1 for rar <= 64)
+  const int bt = warp / wpb, wsl = warp % wpb;
+  const bool bactive = bt < nbt;
+  const int b = bt * 8 + fr;                // this lane's b in A fragments of X^T
+  const int nct = (rbl + 7) / 8, ndt = (rbr + 7) / 8;
+  constexpr int U = 2;  // slices in flight per warp (independent accumulator chains)
+  double acc[U][kG2MaxD][2];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int q = 0; q < kG2MaxD; ++q) acc[u][q][0] = acc[u][q][1] = 0.0;
+
+  for (int c = 0; c < S && c < nch; ++c) issue(c, c);
+  for (int c = 0, st = 0, ph = 0; c < nch; ++c) {
+    const int64_t i0 = s_begin + ((int64_t)c << lns);
+    const int nn = (int)min64(NS, s_end - i0);
+    g2_wait(&bar[st], ph);
+    if (bactive) {
+      const double* xs = Xs + st * xstage + (int64_t)b * a.ldx;
+      const double* ys = Ys + st * ystage;
+      for (int ii0 = wsl; ii0 < nn; ii0 += U * wpb) {
+        bool val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) val[u] = ii0 + u * wpb < nn;
+#pragma unroll 1
+        for (int ct = 0; ct < nct; ++ct) {
+          // Z^T(b, c) tiles for c in [8 ct, 8 ct + 8): K = ral
+          double z[U][2];
+#pragma unroll
+          for (int u = 0; u < U; ++u) z[u][0] = z[u][1] = 0.0;
+          const int cw = ct * 8 + fr;
+          for (int k0 = 0; k0 < ral; k0 += 4) {
+            const int k = k0 + fc;
+            const double wb = (cw < rbl && k < ral) ? Ws[cw + a.ldw * k] : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const double xa = (val[u] && b < rar && k < ral) ? xs[ral * (ii0 + u * wpb) + k] : 0.0;
+              dmma884g(z[u][0], z[u][1], xa, wb);
+            }
+          }
+          // acc(d, b) += Y(c, ii, d) Z(c, ii, b): k = c = 8 ct + 2 fc + h
+          const int c2 = ct * 8 + 2 * fc;
+#pragma unroll
+          for (int dt = 0; dt < kG2MaxD; ++dt) {
+            if (dt >= ndt) break;
+            const int d = dt * 8 + fr;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              double2 yv = make_double2(0.0, 0.0);
+              if (val[u] && d < rbr && c2 < rbl)
+                yv = *reinterpret_cast<const double2*>(ys + (int64_t)d * a.ldy + c2 + rbl * (ii0 + u * wpb));
+              dmma884g(acc[u][dt][0], acc[u][dt][1], yv.x, z[u][0]);
+              dmma884g(acc[u][dt][0], acc[u][dt][1], yv.y, z[u][1]);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage st is free
+    if (c + S < nch) {
+      if (warp == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(c + S, st);
+    }
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+  // reduce the slice shares in a fixed order, write this CTA's partial
+  double* red = Xs;  // wpb x rbr x rar
+  for (int e = tid; e < wpb * rbr * rar; e += kG2NT) red[e] = 0.0;
+  __syncthreads();
+  if (bactive) {
+#pragma unroll
+    for (int dt = 0; dt < kG2MaxD; ++dt) {
+      if (dt >= ndt) break;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = dt * 8 + fr, bb = bt * 8 + 2 * fc + h;
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v += acc[u][dt][h];
+        if (d < rbr && bb < rar) red[(int64_t)wsl * rbr * rar + d + rbr * bb] = v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < rbr * rar; e += kG2NT) {
+    double sum = 0.0;
+    for (int g = 0; g < wpb; ++g) sum += red[(int64_t)g * rbr * rar + e];
+    a.part[(int64_t)blockIdx.x * rbr * rar + e] = sum;
+  }
+}
+
 __global__ void gram_final_kernel(const double* __restrict__ part, int nparts, int cnt, double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += blockDim.x * gridDim.x) {
     double s = 0.0;
@@ -147,6 +341,75 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
   const int64_t cnt = rbr * rar;
   if (I == 0) {
     fill_zero(ctx, Wn, cnt);
+    return;
+  }
+  const bool even = (ral % 2 == 0) && (rbl % 2 == 0) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
+  if (even && getenv("TTB_GRAM_V1") == nullptr) {
+    Gram2Args g;
+    g.W = W;
+    g.X = X;
+    g.Y = Y;
+    g.ral = (int)ral;
+    g.rar = (int)rar;
+    g.rbl = (int)rbl;
+    g.rbr = (int)rbr;
+    g.I = I;
+    g.ldw = g2_ld4((int)rbl);
+    // slices per chunk (a power of two) and stage count: maximise the bytes in
+    // flight ((stages - 1) chunks) within ~220 KB, preferring larger chunks
+    auto stage_bytes = [&](int n) {
+      return ((size_t)rar * g2_ld4((int)ral * n) + (size_t)rbr * g2_ld8((int)rbl * n)) * 8;
+    };
+    auto fixed_bytes = [&](int n) { return ((size_t)48 + (size_t)g.ldw * ral) * 8; };
+    const size_t cap = 220 * 1024;
+    int lns = 0, stages = 2;
+    for (int need = 3; need >= 2; --need) {  // the largest chunk with >= need stages
+      bool found = false;
+      for (int l = 7; l >= 0; --l) {
+        if (l > 0 && (1 << l) > 2 * I) continue;
+        const size_t fb = fixed_bytes(1 << l), sb = stage_bytes(1 << l);
+        if (fb + need * sb > cap) continue;
+        lns = l;
+        stages = (int)std::min<size_t>(8, (cap - fb) / sb);
+        found = true;
+        break;
+      }
+      if (found) break;
+    }
+    if (const char* e = getenv("TTB_GRAM_LNS")) {  // tuning override
+      lns = atoi(e);
+      stages = (int)std::max<size_t>(2, std::min<size_t>(8, (cap - fixed_bytes(1 << lns)) / stage_bytes(1 << lns)));
+    }
+    const int ns = 1 << lns;
+    const int wpb_h = (rbr <= 16 ? 16 : 8) / (int)((rar + 7) / 8);
+    auto bytes = [&](int n) {
+      return std::max(fixed_bytes(n) + (size_t)stages * stage_bytes(n),
+                      fixed_bytes(n) + (size_t)wpb_h * rbr * rar * 8 + 256);
+    };
+    g.lns = lns;
+    g.stages = stages;
+    g.ldx = g2_ld4((int)ral * ns);
+    g.ldy = g2_ld8((int)rbl * ns);
+    const size_t smem = bytes(ns);
+    int grid = (int)std::min<int64_t>((int64_t)ctx.num_sms, (I + ns - 1) / ns);
+    int64_t per_cta = (I + grid - 1) / grid;
+    per_cta = (per_cta + ns - 1) / ns * ns;
+    grid = (int)((I + per_cta - 1) / per_cta);
+    g.per_cta = per_cta;
+    double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
+    g.part = part;
+    ProfScope ps("gram", ctx.stream);
+    auto launch = [&](auto kern, int nt) {
+      TTB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, nt, smem, ctx.stream>>>(g);
+    };
+    if (rbr <= 16) launch(gram2_kernel<2, 512>, 512);
+    else if (rbr <= 32) launch(gram2_kernel<4, 256>, 256);
+    else launch(gram2_kernel<8, 256>, 256);
+    TTB_LAUNCHED();
+    gram_final_kernel<<<(int)std::max<int64_t>(1, (cnt + 255) / 256), 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
+    TTB_LAUNCHED();
+    ctx.free(part);
     return;
   }
   const int64_t per_slice = ral * rar + rbl * rbr + rbl * rar;

@@ -77,9 +77,7 @@ __device__ __forceinline__ void pair_of(int pr, int round, int np, int& p, int& 
 // algorithm); threads [kHalf, kSvdNT) apply each round's rotations to V one
 // round later, off that chain.  Column norms are carried along (updated by
 // each rotation, recomputed exactly at every sweep start), so a pair needs
-// one dot product, not three.  Pairs whose columns are both at roundoff
-// level of the largest column are left alone: rotating them cannot change
-// the result above roundoff.
+// one dot product, not three.
 __global__ void __launch_bounds__(kSvdNT, 1)
 jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int transA, double eps,
                   int max_rank, double* __restrict__ C, double* __restrict__ Vk, double* __restrict__ s_out,
@@ -123,7 +121,13 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     __syncthreads();
     double nmax = 0.0;
     for (int c = 0; c < n; ++c) nmax = fmax(nmax, sm.nrm[c]);
-    const double floor2 = noise2 * nmax;
+    // pairs of columns that are both negligible are left alone: below
+    // roundoff of the largest column, or so small that all of them together
+    // (<= np * eps^2 * 1e-4 / np) sit inside the discarded tail of the
+    // truncation rule -- their mutual rotations cannot change the kept
+    // factors, the kept rank or the discarded-tail sum (rotations that
+    // involve one non-negligible column are still applied)
+    const double floor2 = fmax(noise2 * nmax, eps * eps * 1e-4 / (double)np);
     for (int round = 0; round <= np - 1; ++round) {
       SVD_CLK(0);
       if (!vside) {

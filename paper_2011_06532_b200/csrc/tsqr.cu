@@ -361,35 +361,43 @@ __host__ __device__ __forceinline__ int ldpad(int n) { return ((n + 11) & ~15) +
 // D (optional) multiplies the rows of the root input (sign fix).
 // All three products run on the fp64 MMA path (cta_dmma): W = V_top^T Z,
 // U = T W, z_c = [Z;0]_c - V_c U.
+// One CTA per (node, child): every CTA recomputes the node's small
+// W = V_top^T Z, U = T W (b x b x k each) and writes its own child block,
+// so a node's children are produced in parallel, not one after another.
 __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int nnodes_below, int b, int k,
                                                                    const double* __restrict__ zin,
                                                                    const double* __restrict__ D,
                                                                    double* __restrict__ zout) {
   extern __shared__ __align__(16) double tsm[];
   constexpr int NW = kApplyNT / 32;
-  const int q = blockIdx.x;
+  const int q = blockIdx.x / L.f, c = blockIdx.x - q * L.f;
+  if (q * L.f + c >= nnodes_below) return;
   const int ld = ldpad(b);
   double* Z = tsm;            // b x k (ld)
   double* W = Z + ld * k;     // b x k
   double* U = W + ld * k;     // b x k
-  double* Vb = U + ld * k;    // b x b  (V_top, then each child block)
-  double* Tm = Vb + ld * b;   // b x b
+  double* Vt = U + ld * k;    // b x b  V_top
+  double* Tm = Vt + ld * b;   // b x b
+  double* Vc = Tm + ld * b;   // b x b  this child's block (c > 0)
   const double* Yg = L.Y + (int64_t)q * L.ldy * b;
   const double* Tg = L.T + (int64_t)q * tstride_of(b);
+#pragma unroll 4
   for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
-    const int i = idx % b, c = idx / b;
+    const int i = idx % b, cc = idx / b;
     const double d = D ? D[i] : 1.0;
-    Z[i + ld * c] = d * zin[(int64_t)q * b * k + idx];
+    Z[i + ld * cc] = d * zin[(int64_t)q * b * k + idx];
   }
+#pragma unroll 4
   for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
     const int i = idx % b, j = idx / b;
-    Vb[i + ld * j] = Yg[i + (int64_t)L.ldy * j];
+    Vt[i + ld * j] = Yg[i + (int64_t)L.ldy * j];
     Tm[i + ld * j] = Tg[idx];
+    if (c > 0) Vc[i + ld * j] = Yg[(int64_t)c * b + i + (int64_t)L.ldy * j];
   }
   __syncthreads();
   // W = V_top^T Z  (V_top unit lower: V_top^T(m, l) nonzero for l >= m)
   cta_dmma(
-      b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Vb[l + ld * m] : 0.0; },
+      b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Vt[l + ld * m] : 0.0; },
       [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
       [&](int m, int n, double v) { W[m + ld * n] = v; });
   __syncthreads();
@@ -398,23 +406,14 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int 
       b, k, b, NW, [&](int m, int l) { return (l >= m && l < b && m < b) ? Tm[m + ld * l] : 0.0; },
       [&](int l, int n) { return (l < b && n < k) ? W[l + ld * n] : 0.0; },
       [&](int m, int n, double v) { U[m + ld * n] = v; });
-  const int cnt = min(L.f, nnodes_below - q * L.f);
-  for (int c = 0; c < cnt; ++c) {
-    if (c > 0) {
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
-        const int i = idx % b, j = idx / b;
-        Vb[i + ld * j] = Yg[(int64_t)c * b + i + (int64_t)L.ldy * j];
-      }
-    }
-    __syncthreads();
-    double* zc = zout + ((int64_t)q * L.f + c) * b * k;
-    const bool top = (c == 0);
-    cta_dmma(
-        b, k, b, NW, [&](int m, int l) { return (m < b && l < b) ? Vb[m + ld * l] : 0.0; },
-        [&](int l, int n) { return (l < b && n < k) ? U[l + ld * n] : 0.0; },
-        [&](int m, int n, double v) { zc[m + b * n] = (top ? Z[m + ld * n] : 0.0) - v; });
-  }
+  __syncthreads();
+  double* zc = zout + ((int64_t)q * L.f + c) * b * k;
+  const double* V = c == 0 ? Vt : Vc;
+  const bool top = (c == 0);
+  cta_dmma(
+      b, k, b, NW, [&](int m, int l) { return (m < b && l < b) ? V[m + ld * l] : 0.0; },
+      [&](int l, int n) { return (l < b && n < k) ? U[l + ld * n] : 0.0; },
+      [&](int m, int n, double v) { zc[m + b * n] = (top ? Z[m + ld * n] : 0.0) - v; });
 }
 
 // ---- 2. chains ------------------------------------------------------------
@@ -838,13 +837,13 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   const double* Dp = f.D;
   int which = 0;
   const int ldb = ldpad(b);
-  const size_t tsmem = (size_t)(3 * (int64_t)ldb * k + 2 * (int64_t)ldb * b) * sizeof(double);
+  const size_t tsmem = (size_t)(3 * (int64_t)ldb * k + 3 * (int64_t)ldb * b) * sizeof(double);
   // global levels (redundant on every rank), then this rank's block
   for (int L = (int)gnodes.size() - 1; L >= 0; --L) {
     const int below = L == 0 ? ctx.nranks : gnodes[L - 1];
     Level lv{f.gloY[L], f.gloT[L], f.ldy_tree, f.ftree, -1};
     ProfScope ps("apply_tree", ctx.stream);
-    tsqr_tree_apply_kernel<<<gnodes[L], kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
+    tsqr_tree_apply_kernel<<<gnodes[L] * f.ftree, kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
     TTB_LAUNCHED();
     Dp = nullptr;
     cur = lev[which] + (L == 0 ? (int64_t)ctx.rank * bk : 0);
@@ -854,7 +853,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
     const int below = L == 0 ? G : lnodes[L - 1];
     Level lv{f.locY[L], f.locT[L], f.ldy_tree, f.ftree, -1};
     ProfScope ps("apply_tree", ctx.stream);
-    tsqr_tree_apply_kernel<<<lnodes[L], kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
+    tsqr_tree_apply_kernel<<<lnodes[L] * f.ftree, kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
     TTB_LAUNCHED();
     Dp = nullptr;
     cur = lev[which];

@@ -150,15 +150,15 @@ constexpr int kRing = 4;  // Householder vectors in flight between warps
 // Debug-only cycle stamps of the column pipeline (CTA 0, second tile):
 // build with NVCC_EXTRA=-DTTB_DEBUG_CLK, read back with ttb_dbg_clk.
 #ifdef TTB_DEBUG_CLK
-static __device__ long long g_dclk[8 * 64 * 8];
+static __device__ long long g_dclk[16 * 64 * 8];
 #define TTB_DCLK(ph)                                                                     \
   do {                                                                                   \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && gbase == b && j < 64 && threadIdx.x < 256) \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && gbase == b && j < 64 && threadIdx.x < 512) \
       g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                      \
   } while (0)
 #define TTB_DCLK2(ph)                                                                        \
   do {                                                                                       \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gj - j) > 0 && (gj - j) <= 64 && j < 64 && threadIdx.x < 256) \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gj - j) > 0 && (gj - j) <= 64 && j < 64 && threadIdx.x < 512) \
       g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                          \
   } while (0)
 #else
@@ -203,10 +203,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
   unsigned done = 0;
   do {
     asm volatile(
+#ifdef TTB_MBAR_HINT
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(TTB_MBAR_HINT)
+        : "memory");
+#else
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#endif
   } while (!done);
 }
 
@@ -449,6 +456,9 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
     double p[CPL], q[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
+#ifdef TTB_EXPT_NODOT  // timing experiment only
+      if (!producer) { p[t] = 0.0; q[t] = 0.0; continue; }
+#endif
       double a0 = 0.0, a1 = 0.0, qa = 0.0;
 #pragma unroll
       for (int s = 0; s < RPL; ++s) {
@@ -494,10 +504,12 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
     }
+#ifndef TTB_EXPT_NOUPD  // timing experiment only: skip the off-critical-path updates
     if (tn != 0) TTB_UPD(0);
     if (CPL > 1 && tn != 1) TTB_UPD(T1);
     if (CPL > 2 && tn != 2) TTB_UPD((kSlot<C, 2>));
     if (CPL > 3 && tn != 3) TTB_UPD((kSlot<C, 3>));
+#endif
 #undef TTB_UPD
 #pragma unroll
     for (int t = 0; t < CPL; ++t)
