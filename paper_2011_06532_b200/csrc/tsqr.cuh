@@ -176,7 +176,7 @@ struct TileSmem {
   double Gs[C::BMAX * C::BMAX];      // V^T V strict upper -> T after inversion
   double Xs[C::BMAX * C::BMAX / 2];  // inversion scratch
   double vring[kRing][C::MC];        // published raw columns
-  double sc[kRing][4];               // published tau, scal, beta
+  alignas(16) double sc[kRing][4];   // published tau, scal, bv, beta
   double taus[C::BMAX];
   unsigned long long full[kRing];    // raw column ready (count 1)
   unsigned long long fulls[kRing];   // scalars ready (count 1)
@@ -274,6 +274,39 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
 // (body), consumers compute p = x . a (and q = a_j for head tiles) while the
 // scalars are still in flight, and only then finish d = v . a and the update
 // a -= tau d v.  sqrt/div leave the column-to-column critical path.
+// Reflector scalars from alpha (pivot) and sig (squared norm below it):
+// beta = -sign(alpha) |(alpha, x)|, tau = 1 + |alpha| / |(alpha, x)|,
+// scal = 1 / (alpha - beta) (v = scal (x - bv e_j) for head tiles, [e_j; scal x]
+// for body tiles).  sig == 0 reflects e_j onto -e_j (tau = 2, keeps tau in
+// [1, 2]); bv differs from beta only for an all-zero head column (v = e_j).
+// One rsqrt and one reciprocal, no divides.  Bitwise identical wherever it
+// is evaluated from the same (alpha, sig).
+template <bool HEAD>
+__device__ __forceinline__ void reflector_scalars(double alpha, double sig, double& beta, double& tau, double& scal,
+                                                  double& bv) {
+  if (sig == 0.0) {
+    beta = -alpha;
+    tau = 2.0;
+    if (HEAD && alpha == 0.0) {
+      scal = 1.0;
+      bv = -1.0;
+    } else {
+      scal = HEAD ? 0.5 / alpha : 0.0;
+      bv = beta;
+    }
+  } else {
+    const double n2 = fma(alpha, alpha, sig);
+    const double rn = rsqrt(n2);
+    const double nrm = n2 * rn;
+    const double den = fabs(alpha) + nrm;
+    const double rden = __drcp_rn(den);
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = den * rn;
+    scal = alpha >= 0.0 ? rden : -rden;
+    bv = beta;
+  }
+}
+
 template <class C, bool HEAD, int OT>
 __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j, int gj, TileSmem<C>& sm) {
   constexpr int LR = C::LR, RPL = C::RPL, BM = C::BMAX;
@@ -281,6 +314,7 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
   const int lc = lane / LR, lr = lane % LR;
   const bool mine = (lc == C::owner_lc(j));
   const int slot = gj % kRing;
+  const double alpha_r = HEAD ? 0.0 : sm.Rs[j + BM * j];  // prefetched: it heads the scalar chain
   // 1. raw column
   if (mine) {
     double* xb = sm.vring[slot];
@@ -298,7 +332,7 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
   if (lane == 0) mbar_arrive(&sm.full[slot]);
   TTB_DCLK2(4);
   // 2. scalars
-  double sig0 = 0.0, sig1 = 0.0, aj = 0.0;
+  double sg[4] = {0.0, 0.0, 0.0, 0.0}, aj = 0.0;
 #pragma unroll
   for (int s = 0; s < RPL; ++s) {
     double x = A[s][OT];
@@ -307,46 +341,26 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
       if (r == j) aj = x;
       x = r > j ? x : 0.0;
     }
-    if (s & 1) sig1 = fma(x, x, sig1); else sig0 = fma(x, x, sig0);
+    sg[s & 3] = fma(x, x, sg[s & 3]);
   }
-  double sig = sig0 + sig1;
+  double sig = (sg[0] + sg[1]) + (sg[2] + sg[3]);
 #pragma unroll
   for (int off = LR / 2; off > 0; off >>= 1) {
     sig += __shfl_xor_sync(0xffffffffu, sig, off);
     if (HEAD) aj += __shfl_xor_sync(0xffffffffu, aj, off);
   }
   TTB_DCLK2(5);
-  const double alpha = HEAD ? aj : sm.Rs[j + BM * j];
-  // bv: the beta used in v = scal (x - bv e_j); equals beta except for an
-  // all-zero head column, where v = e_j must come from bv = -1, scal = 1.
+  const double alpha = HEAD ? aj : alpha_r;
   double beta, tau, scal, bv;
-  if (sig == 0.0) {  // reflect e_j onto -e_j: keeps tau in [1, 2] always
-    beta = -alpha;
-    tau = 2.0;
-    if (HEAD && alpha == 0.0) {
-      scal = 1.0; bv = -1.0;
-    } else {
-      scal = HEAD ? 0.5 / alpha : 0.0; bv = beta;
-    }
-  } else {
-    // nu = sqrt(alpha^2 + sig); beta = -sign(alpha) nu
-    // tau = (beta - alpha)/beta = 1 + |alpha|/nu ; scal = 1/(alpha - beta)
-    const double nrm = sqrt(fma(alpha, alpha, sig));
-    const double den = fabs(alpha) + nrm;
-    const double rden = 1.0 / den;
-    beta = alpha >= 0.0 ? -nrm : nrm;
-    tau = den / nrm;
-    scal = alpha >= 0.0 ? rden : -rden;
-    bv = beta;
-  }
+  reflector_scalars<HEAD>(alpha, sig, beta, tau, scal, bv);
   TTB_DCLK2(6);
   if (mine && lr == 0) {  // the owner group holds this column's sigma / alpha
-    sm.sc[slot][0] = tau;
-    sm.sc[slot][1] = scal;
-    sm.sc[slot][2] = bv;
-    sm.taus[j] = tau;
-    if (!HEAD) sm.Rs[j + BM * j] = beta;
+    double2* scp = reinterpret_cast<double2*>(sm.sc[slot]);
+    scp[0] = make_double2(tau, scal);
+    scp[1] = make_double2(bv, beta);
     mbar_arrive(&sm.fulls[slot]);
+    sm.taus[j] = tau;  // off the chain: read at the end of the tile
+    if (!HEAD) sm.Rs[j + BM * j] = beta;
   }
   TTB_DCLK2(7);
   // 3. own column becomes the stored Householder vector (R on top for head)
@@ -478,13 +492,13 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
     }
     if (producer && gj + 1 >= kRing) mbar_wait(&sm.empty[(gj + 1) % kRing], (((gj + 1) / kRing) - 1) & 1);
     mbar_wait(&sm.fulls[slot], (gj / kRing) & 1);
+    const double2 sc01 = *reinterpret_cast<const double2*>(&sm.sc[slot][0]);
+    const double2 sc23 = *reinterpret_cast<const double2*>(&sm.sc[slot][2]);
+    const double tau = sc01.x, scal = sc01.y, beta = sc23.x;
     TTB_DCLK(2);
-    const double tau = sm.sc[slot][0], scal = sm.sc[slot][1], beta = sm.sc[slot][2];
     double rjk[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; ++t) rjk[t] = (!HEAD && kk[t] > j && kk[t] < b) ? sm.Rs[j + BM * kk[t]] : 0.0;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);
     double d[CPL], c[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
@@ -504,6 +518,8 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
     }
+    __syncwarp();  // slot gj consumed by every lane of this warp (x and scalars are in registers)
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
 #ifndef TTB_EXPT_NOUPD  // timing experiment only: skip the off-critical-path updates
     if (tn != 0) TTB_UPD(0);
     if (CPL > 1 && tn != 1) TTB_UPD(T1);
