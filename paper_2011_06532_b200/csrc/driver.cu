@@ -410,21 +410,41 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   meta[1] = eps;
 
   // ---- truncation sweep ----
+  // The output core of step n (Q2 V, from this step's TSQR factor and SVD)
+  // is off the critical path: it is computed on the side stream, deferred
+  // until the next step's TSQR has been enqueued, so that it runs while the
+  // main stream sits in the one-CTA SVD instead of competing with the
+  // critical carry apply.
   bool violated = false;
   Ctx sctx = ctx;
   sctx.stream = ctx.side_stream();
+  struct Deferred {
+    bool on = false;
+    Tsqr f2;
+    SvdOut so;
+    Panel out;
+    int n = 0;
+    int64_t count = 0;
+  } pend;
+  auto flush = [&]() {
+    if (!pend.on) return;
+    side_begin(ctx, sctx);  // after everything enqueued on main so far
+    tsqr_apply(sctx, pend.f2, pend.so.Vk, pend.so.keep, pend.out);
+    if (io) io->ready(pend.n, pend.out.base, pend.count, sctx.stream);
+    tsqr_release(sctx, pend.f2);
+    sctx.free(pend.so.mem);
+    pend.on = false;
+  };
   if (left_first) {
     for (int n = N - 1; n >= 1; --n) {
       const int b = (int)r[n];
       Tsqr f2;
       tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2);
+      flush();  // previous step's output core overlaps this step's SVD
       SvdOut so;
       svd_of_rt(ctx, f2.R, b, eps, mr, so);
       const int keep = so.keep;
       violated |= so.capped != 0;
-      // output core n = (Q2 V)^T: off the critical path, on the side stream
-      side_begin(ctx, sctx);
-      tsqr_apply(sctx, f2, so.Vk, keep, panel_of(out[n], keep, d[n], r[n + 1], 1));
       if (implicit) {
         tsqr_apply(ctx, facs[n - 1], so.C, keep, panel_of(out[n - 1], r[n - 1], d[n - 1], keep, 0));
         tsqr_release(ctx, facs[n - 1]);
@@ -433,22 +453,26 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
         gemm_small_right(ctx, Mb, b, keep, out[n - 1], so.C, b, false, scratch);
         copy_d2d(ctx, out[n - 1], scratch, Mb * keep);
       }
-      if (io) io->ready(n, out[n], (int64_t)keep * d[n] * r[n + 1], sctx.stream);
-      side_end(ctx, sctx, f2, so.mem);
+      pend.on = true;
+      pend.f2 = f2;
+      pend.so = so;
+      pend.out = panel_of(out[n], keep, d[n], r[n + 1], 1);
+      pend.n = n;
+      pend.count = (int64_t)keep * d[n] * r[n + 1];
       r[n] = keep;
     }
+    flush();
     if (io) io->ready(0, out[0], r[0] * d[0] * r[1], ctx.stream);
   } else {
     for (int n = 0; n < N - 1; ++n) {
       const int b = (int)r[n + 1];
       Tsqr f2;
       tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 0), f2);
+      flush();
       SvdOut so;
       svd_of_rt(ctx, f2.R, b, eps, mr, so);
       const int keep = so.keep;
       violated |= so.capped != 0;
-      side_begin(ctx, sctx);
-      tsqr_apply(sctx, f2, so.Vk, keep, panel_of(out[n], r[n], d[n], keep, 0));
       if (implicit) {
         tsqr_apply(ctx, facs[n + 1], so.C, keep, panel_of(out[n + 1], keep, d[n + 1], r[n + 2], 1));
         tsqr_release(ctx, facs[n + 1]);
@@ -457,10 +481,15 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
         gemm_small_left(ctx, keep, b, Nb, so.C, b, true, out[n + 1], scratch);
         copy_d2d(ctx, out[n + 1], scratch, keep * Nb);
       }
-      if (io) io->ready(n, out[n], r[n] * d[n] * (int64_t)keep, sctx.stream);
-      side_end(ctx, sctx, f2, so.mem);
+      pend.on = true;
+      pend.f2 = f2;
+      pend.so = so;
+      pend.out = panel_of(out[n], r[n], d[n], keep, 0);
+      pend.n = n;
+      pend.count = r[n] * d[n] * (int64_t)keep;
       r[n + 1] = keep;
     }
+    flush();
     if (io) io->ready(N - 1, out[N - 1], r[N - 1] * d[N - 1] * r[N], ctx.stream);
   }
   side_join(ctx, sctx);
