@@ -96,6 +96,132 @@ static void launch_skinny(Ctx& ctx, const SkinnyArgs& a) {
   TTB_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// Left fold on a persistent, bulk-copy pipelined kernel: B = H (K x N,
+// column-major, ld K) is streamed in chunks of kFoldJ columns -- one
+// contiguous block, one bulk copy (TMA engine) each, kFoldStages - 1 chunks
+// in flight -- and multiplied by the small operand held in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kFoldJ = 64;
+constexpr int kFoldStages = 5;
+constexpr int kFoldNT = 256;
+
+__device__ __forceinline__ unsigned fd_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(kFoldNT, 1) fold_left_kernel(SkinnyArgs a) {
+  extern __shared__ __align__(128) double fsm[];
+  constexpr int NW = kFoldNT / 32;
+  const int M = a.M, K = a.K;
+  const int64_t N = a.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int ldS = ((K + 11) & ~15) + 4;  // >= K, 4 mod 16
+  const int MP = (M + 15) & ~15, KP = (K + 3) & ~3;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(fsm);
+  double* Ss = fsm + 16;                          // MP x ldS (row m)
+  double* Bs = Ss + (int64_t)MP * ldS;            // stages of K x kFoldJ
+  Bs += (16 - ((Bs - fsm) & 15)) & 15;
+  const int64_t bstage = (int64_t)K * kFoldJ;
+  if (tid < kFoldStages) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fd_smem(&bar[tid])) : "memory");
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  for (int idx = tid; idx < MP * ldS; idx += kFoldNT) {
+    const int m = idx / ldS, k = idx % ldS;
+    Ss[idx] = (m < M && k < K) ? a.S[m * a.ssm + k * a.ssk] : 0.0;
+  }
+  const int64_t nch = (N + kFoldJ - 1) / kFoldJ;
+  __syncthreads();
+  auto issue = [&](int64_t c, int st) {
+    if (tid != 0) return;
+    const int64_t j0 = c * kFoldJ;
+    const int nj = (int)min64(kFoldJ, N - j0);
+    const unsigned bytes = (unsigned)(K * nj * 8);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     fd_smem(Bs + st * bstage)),
+                 "l"(a.B + K * j0), "r"(bytes), "r"(fd_smem(&bar[st]))
+                 : "memory");
+  };
+  int st = 0, ph = 0, fill = 0;
+  for (int64_t c = blockIdx.x; c < nch && fill < kFoldStages; c += gridDim.x, ++fill) issue(c, fill);
+  const int mt = MP / 16, ntl = kFoldJ / 16;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const int64_t j0 = c * kFoldJ;
+    const int nj = (int)min64(kFoldJ, N - j0);
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(fd_smem(&bar[st])), "r"(ph)
+          : "memory");
+    } while (!done);
+    const double* bs = Bs + st * bstage;
+    for (int blk = warp; blk < mt * ntl; blk += NW) {
+      const int m0 = (blk % mt) * 16, n0 = (blk / mt) * 16;
+      double acc[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const bool c0 = n0 + fr < nj, c1 = n0 + 8 + fr < nj;
+      const double* b0p = bs + (int64_t)K * (n0 + fr);
+      const double* b1p = bs + (int64_t)K * (n0 + 8 + fr);
+      const double* a0p = Ss + (int64_t)(m0 + fr) * ldS;
+      const double* a1p = Ss + (int64_t)(m0 + 8 + fr) * ldS;
+#pragma unroll 4
+      for (int k0 = 0; k0 < KP; k0 += 4) {
+        const int k = k0 + fc;
+        const bool kin = k < K;
+        const double a0 = a0p[k], a1 = a1p[k];  // zero padded
+        const double b0 = (c0 && kin) ? b0p[k] : 0.0;
+        const double b1 = (c1 && kin) ? b1p[k] : 0.0;
+        dmma_884(acc[0][0][0], acc[0][0][1], a0, b0);
+        dmma_884(acc[0][1][0], acc[0][1][1], a0, b1);
+        dmma_884(acc[1][0][0], acc[1][0][1], a1, b0);
+        dmma_884(acc[1][1][0], acc[1][1][1], a1, b1);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = m0 + 8 * i + fr, n = n0 + 8 * jj + 2 * fc + h;
+            if (m < M && n < nj) a.O[m + (int64_t)M * (j0 + n)] = acc[i][jj][h];
+          }
+    }
+    __syncthreads();  // stage st consumed
+    const int64_t nxt = c + (int64_t)kFoldStages * gridDim.x;
+    if (nxt < nch) {
+      if (tid == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(nxt, st);
+    }
+    if (++st == kFoldStages) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+static bool fold_left_tma(Ctx& ctx, const SkinnyArgs& a) {
+  // bulk copies need 16-byte sizes / addresses: K * columns even, aligned base
+  if (a.K % 2 != 0 || ((uintptr_t)a.B & 15) || a.N < (int64_t)kFoldJ * ctx.num_sms) return false;
+  const int ldS = ((a.K + 11) & ~15) + 4, MP = (a.M + 15) & ~15;
+  const size_t smem = (16 + (size_t)MP * ldS + 16 + (size_t)kFoldStages * a.K * kFoldJ) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    TTB_CUDA(cudaFuncSetAttribute(fold_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  if (smem > 227 * 1024) return false;
+  const int64_t nch = (a.N + kFoldJ - 1) / kFoldJ;
+  const int grid = (int)std::min<int64_t>(nch, ctx.num_sms);
+  fold_left_kernel<<<grid, kFoldNT, smem, ctx.stream>>>(a);
+  TTB_LAUNCHED();
+  return true;
+}
+
 // out_H (M x N) = F (M x K) * H (K x N); H col-major ld K, out col-major ld M
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
                      double* out) {
@@ -113,6 +239,7 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
   a.O = out;
   a.osm = 1;
   a.osj = M;
+  if (getenv("TTB_FOLD_V1") == nullptr && fold_left_tma(ctx, a)) return;
   launch_skinny(ctx, a);
 }
 
