@@ -77,12 +77,15 @@ class Clocks:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, enabled=True):
         self.index = index
+        self.enabled = enabled
         self.lines = []
         self.proc = None
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -211,7 +214,7 @@ def run_ours(args):
     l0 = _lib.launch_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(local, enabled=os.environ.get("TTB_BENCH_NO_SMI") is None) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             out = T.round_tt(x, opts)
