@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 
@@ -64,10 +65,15 @@ static void nccl_check(int rc, const char* what) {
 static constexpr int kNcclDouble = 8;  // ncclFloat64
 static constexpr int kNcclSum = 0;     // ncclSum
 
+double g_host_alloc_ms = 0.0;  // diagnostics (TTB_DEBUG_HOSTTIME)
+
 void* Ctx::alloc(size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 256;
+  if (!deferred.empty()) collect(false);
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  g_host_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (e != cudaSuccess) {
     cudaGetLastError();
     TTB_THROW(TTB_ERR_CAPACITY, std::string("device allocation of ") + std::to_string(bytes) +
@@ -78,6 +84,31 @@ void* Ctx::alloc(size_t bytes) {
 
 void Ctx::free(void* p) {
   if (p) TTB_CUDA(cudaFreeAsync(p, stream));
+}
+
+void Ctx::free_after(void* p, cudaStream_t used_on) {
+  if (!p) return;
+  cudaEvent_t e;
+  TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TTB_CUDA(cudaEventRecord(e, used_on));
+  deferred.push_back({p, e});
+}
+
+void Ctx::collect(bool all) {
+  size_t keep = 0;
+  for (size_t i = 0; i < deferred.size(); ++i) {
+    Deferred d = deferred[i];
+    const cudaError_t q = all ? cudaSuccess : cudaEventQuery(d.ev);
+    if (q == cudaSuccess) {
+      TTB_CUDA(cudaStreamWaitEvent(stream, d.ev, 0));
+      TTB_CUDA(cudaFreeAsync(d.p, stream));
+      cudaEventDestroy(d.ev);
+    } else {
+      if (q != cudaErrorNotReady) TTB_CUDA(q);
+      deferred[keep++] = d;
+    }
+  }
+  deferred.resize(keep);
 }
 
 void Ctx::allgather(const double* send, double* recv, size_t count) {
@@ -95,6 +126,46 @@ void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }
 cudaStream_t Ctx::side_stream() {
   if (!side) TTB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   return side;
+}
+
+__global__ void read_small_kernel(const unsigned char* __restrict__ src, volatile unsigned char* dst, int bytes,
+                                  volatile unsigned* flag, unsigned seq) {
+  for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *flag = seq;
+  }
+}
+
+// The host spins on the flag word instead of blocking in
+// cudaStreamSynchronize: blocking waits can take milliseconds to wake in a
+// virtualised host, and the rounding sweep reads a rank back after every
+// truncated SVD.  cudaStreamQuery is polled now and then so launch or
+// kernel errors surface instead of spinning forever.
+void Ctx::read_small(const void* dev, size_t bytes, void* host) {
+  TTB_CHECK(bytes <= 256, TTB_ERR_CONTRACT, "read_small: at most 256 bytes");
+  if (!mapped_host) {
+    TTB_CUDA(cudaHostAlloc(&mapped_host, 512, cudaHostAllocMapped));
+    TTB_CUDA(cudaHostGetDevicePointer(&mapped_dev, mapped_host, 0));
+    memset(mapped_host, 0, 512);
+  }
+  volatile unsigned* hflag = reinterpret_cast<volatile unsigned*>((char*)mapped_host + 256);
+  unsigned* dflag = reinterpret_cast<unsigned*>((char*)mapped_dev + 256);
+  const unsigned seq = ++read_seq;
+  read_small_kernel<<<1, 32, 0, stream>>>((const unsigned char*)dev, (volatile unsigned char*)mapped_dev, (int)bytes,
+                                          dflag, seq);
+  TTB_LAUNCHED();
+  for (long spin = 0; *hflag != seq; ++spin) {
+    if ((spin & 0xFFFF) == 0xFFFF) {
+      const cudaError_t q = cudaStreamQuery(stream);
+      if (q == cudaSuccess) break;  // completed (flag visibility lagging)
+      if (q != cudaErrorNotReady) TTB_CUDA(q);
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  memcpy(host, mapped_host, bytes);
 }
 
 cudaStream_t Ctx::copy_stream() {
@@ -147,6 +218,7 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
     if (ctx->c.nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->c.nccl_comm);
     if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
     if (ctx->c.copy) cudaStreamDestroy(ctx->c.copy);
+    if (ctx->c.mapped_host) cudaFreeHost(ctx->c.mapped_host);
     delete ctx;
   }
   TTB_TRY_END

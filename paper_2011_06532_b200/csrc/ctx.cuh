@@ -4,12 +4,15 @@
 // pin a second libnccl next to the one torch loads.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 #include "tsqr.cuh"
 
 namespace ttb {
 
 struct NcclApi;  // defined in ctx.cu
+extern double g_host_alloc_ms;  // diagnostics: host time in cudaMallocAsync
 
 struct Ctx {
   int device = 0;
@@ -24,8 +27,26 @@ struct Ctx {
   cudaStream_t side_stream();
   cudaStream_t copy = nullptr;  // host<->device transfers of the host API (lazily created)
   cudaStream_t copy_stream();
+  // small device -> host reads (ranks, norms) go through mapped pinned
+  // memory written by a kernel: they never queue behind bulk DMA copies
+  // (e.g. the host API's output downloads on the copy engine)
+  void* mapped_host = nullptr;
+  void* mapped_dev = nullptr;
+  unsigned read_seq = 0;
+  void read_small(const void* dev, size_t bytes, void* host);
   void* alloc(size_t bytes);
   void free(void* p);
+  // free memory last used on another stream: the block goes back to the
+  // pool on THIS stream once that use has completed (checked at later
+  // allocations), so the stream-ordered pool never has to pick between
+  // cross-stream reuse and growth
+  void free_after(void* p, cudaStream_t used_on);
+  void collect(bool all);
+  struct Deferred {
+    void* p;
+    cudaEvent_t ev;
+  };
+  std::vector<Deferred> deferred;
   // collectives on this->stream (nranks > 1 only)
   void allgather(const double* send, double* recv, size_t count);
   void allreduce_sum(const double* send, double* recv, size_t count);

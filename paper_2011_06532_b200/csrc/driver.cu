@@ -1,3 +1,4 @@
+#include <chrono>
 // Native drivers behind the C ABI (include/ttb.h): TT construction, Gram
 // sweeps, orthonormalization and the four rounding variants.  These replace
 // the reference's Python sweep loops (parallel.py:164-209, 293-438;
@@ -54,8 +55,7 @@ static void check_chain(int ndim, const int64_t* dims, const int64_t* ranks) {
 
 static double host_scalar(Ctx& ctx, const double* d) {
   double h = 0.0;
-  TTB_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  ctx.sync();
+  ctx.read_small(d, sizeof(double), &h);
   return h;
 }
 
@@ -79,16 +79,6 @@ static void side_begin(Ctx& ctx, Ctx& sctx) {
   TTB_CUDA(cudaEventRecord(e, ctx.stream));
   TTB_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
   TTB_CUDA(cudaEventDestroy(e));
-}
-
-static void side_end(Ctx& ctx, Ctx& sctx, Tsqr& f2, void* svdmem) {
-  cudaEvent_t e;
-  TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  TTB_CUDA(cudaEventRecord(e, ctx.stream));      // main's use of the SVD outputs
-  TTB_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
-  TTB_CUDA(cudaEventDestroy(e));
-  tsqr_release(sctx, f2);
-  sctx.free(svdmem);
 }
 
 static void side_join(Ctx& ctx, Ctx& sctx) {
@@ -121,8 +111,7 @@ static void svd_of_rt(Ctx& ctx, const double* R, int b, double eps, int max_rank
   o.info = (int*)(o.dinfo + 1);
   jacobi_svd(ctx, R, b, b, b, true, eps, max_rank, o.C, o.Vk, o.s, o.info, o.dinfo);
   int hinfo[4] = {0, 0, 0, 0};
-  TTB_CUDA(cudaMemcpyAsync(hinfo, o.info, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  ctx.sync();
+  ctx.read_small(o.info, 4 * sizeof(int), hinfo);
   prof_note("svd_sweeps", hinfo[3]);
   TTB_CHECK(hinfo[2] == 0, TTB_ERR_NUMERIC, "non-finite entries in SVD input");
   o.keep = hinfo[0];
@@ -296,15 +285,25 @@ struct HostIO {
     TTB_CUDA(cudaStreamWaitEvent(st, in_ev[n], 0));
     waited[n] = 1;
   }
+  struct Late { int n; const double* src; int64_t count; };
+  std::vector<Late> late;
   void ready(int n, const double* src, int64_t count, cudaStream_t st) {
     cudaEvent_t e;
     TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     TTB_CUDA(cudaEventRecord(e, st));
     TTB_CUDA(cudaStreamWaitEvent(cs(), e, 0));
     evs.push_back(e);
+    static const bool late_d2h = getenv("TTB_HOSTIO_LATE_D2H") != nullptr;  // diagnostics
+    if (late_d2h) {
+      late.push_back({n, src, count});
+      return;
+    }
     TTB_CUDA(cudaMemcpyAsync(hout[n], src, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, cs()));
   }
   void finish() {
+    for (auto& l : late)
+      cudaMemcpyAsync(hout[l.n], l.src, (size_t)l.count * sizeof(double), cudaMemcpyDeviceToHost, cs());
+    late.clear();
     // the compute stream must not run past the copies (device buffers are
     // freed stream-ordered on it), and the caller reads host memory
     cudaEvent_t e;
@@ -324,10 +323,30 @@ struct HostIO {
   }
 };
 
+
+struct HostTimer {  // diagnostics: TTB_DEBUG_HOSTTIME prints host-side phase times per round
+  const char* name;
+  double* acc;
+  std::chrono::steady_clock::time_point t0;
+  HostTimer(const char* n, double* a) : name(n), acc(a), t0(std::chrono::steady_clock::now()) {}
+  ~HostTimer() { *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+};
+
 static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
                        const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks,
                        double* meta, HostIO* io) {
   check_chain(ndim, dims, ranks);
+  static const bool htime = getenv("TTB_DEBUG_HOSTTIME") != nullptr;
+  double t_all = 0, t_fac = 0, t_svd = 0, t_app = 0, t_flush = 0, t_norm = 0;
+  const double alloc0 = g_host_alloc_ms;
+  struct Report {
+    bool on; double *a, *f, *s, *p, *fl, *nm; double alloc0;
+    ~Report() {
+      if (on)
+        fprintf(stderr, "[hosttime] factor %.2f svd %.2f apply %.2f flush %.2f norm %.2f alloc %.2f ms\n", *f, *s, *p, *fl,
+                *nm, g_host_alloc_ms - alloc0);
+    }
+  } rep{htime, &t_all, &t_fac, &t_svd, &t_app, &t_flush, &t_norm, alloc0};
   TTB_CHECK(variant >= 0 && variant <= 3, TTB_ERR_CONTRACT, "unknown rounding variant");
   TTB_CHECK(eps0 >= 0.0, TTB_ERR_CONTRACT, "eps0 must be nonnegative");
   const int N = ndim;
@@ -360,7 +379,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
       const double* src = (n == 0) ? in[0] : out[n];
       const int b = (int)r[n + 1];
       if (io && n == 0) io->need(0, ctx.stream);
-      tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 0), facs[n]);
+      { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 0), facs[n]); }
       if (io) io->need(n + 1, ctx.stream);
       if (!implicit) {
         double* eye = make_eye(ctx, b);
@@ -392,7 +411,8 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   }
 
   // ---- norm and per-bond threshold ----
-  const double nx = std::sqrt(std::max(global_sumsq(ctx, last_n, last), 0.0));
+  double nx;
+  { HostTimer ht("norm", &t_norm); nx = std::sqrt(std::max(global_sumsq(ctx, last_n, last), 0.0)); }
   meta[0] = nx;
   if (nx < 1e-300) {
     for (int n = 0; n < N; ++n) {
@@ -418,6 +438,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   bool violated = false;
   Ctx sctx = ctx;
   sctx.stream = ctx.side_stream();
+  sctx.deferred.clear();  // deferred frees belong to the main context only
   struct Deferred {
     bool on = false;
     Tsqr f2;
@@ -431,21 +452,23 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     side_begin(ctx, sctx);  // after everything enqueued on main so far
     tsqr_apply(sctx, pend.f2, pend.so.Vk, pend.so.keep, pend.out);
     if (io) io->ready(pend.n, pend.out.base, pend.count, sctx.stream);
-    tsqr_release(sctx, pend.f2);
-    sctx.free(pend.so.mem);
+    ctx.free_after(pend.f2.mem, sctx.stream);  // returned to the pool on the main stream
+    pend.f2.mem = nullptr;
+    ctx.free_after(pend.so.mem, sctx.stream);
     pend.on = false;
   };
   if (left_first) {
     for (int n = N - 1; n >= 1; --n) {
       const int b = (int)r[n];
       Tsqr f2;
-      tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2);
-      flush();  // previous step's output core overlaps this step's SVD
+      { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2); }
+      { HostTimer ht("flush", &t_flush); flush(); }  // previous step's output core overlaps this step's SVD
       SvdOut so;
-      svd_of_rt(ctx, f2.R, b, eps, mr, so);
+      { HostTimer ht("svd", &t_svd); svd_of_rt(ctx, f2.R, b, eps, mr, so); }
       const int keep = so.keep;
       violated |= so.capped != 0;
       if (implicit) {
+        HostTimer ht("app", &t_app);
         tsqr_apply(ctx, facs[n - 1], so.C, keep, panel_of(out[n - 1], r[n - 1], d[n - 1], keep, 0));
         tsqr_release(ctx, facs[n - 1]);
       } else {
@@ -493,6 +516,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     if (io) io->ready(N - 1, out[N - 1], r[N - 1] * d[N - 1] * r[N], ctx.stream);
   }
   side_join(ctx, sctx);
+  ctx.collect(true);
   if (scratch) ctx.free(scratch);
   meta[2] = violated ? 1.0 : 0.0;
   for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
@@ -512,6 +536,14 @@ int ttb_round_host(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int n
   Ctx& ctx = h->c;
   check_chain(ndim, dims, ranks);
   TTB_CHECK(in && out, TTB_ERR_CONTRACT, "null core pointer array");
+  static const bool dbg = getenv("TTB_DEBUG_HOSTIO") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(ctx.stream);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[hostio] %-28s %8.2f ms\n", what, ms);
+  };
   std::vector<int64_t> sz(ndim);
   int64_t total = 0;
   for (int n = 0; n < ndim; ++n) {
@@ -537,7 +569,9 @@ int ttb_round_host(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int n
     TTB_CUDA(cudaStreamWaitEvent(io.cs(), e, 0));
     TTB_CUDA(cudaEventDestroy(e));
   }
+  mark("alloc");
   for (int n = 0; n < ndim; ++n) io.upload(n, const_cast<double*>(din[n]), sz[n]);
+  mark("uploads queued");
   try {
     round_impl(ctx, variant, eps0, max_rank, ndim, dims, ranks, din.data(), dout.data(), out_ranks, meta, &io);
   } catch (...) {
@@ -545,7 +579,9 @@ int ttb_round_host(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int n
     ctx.free(dmem);
     throw;
   }
+  mark("round done (compute stream)");
   io.finish();
+  mark("copies done");
   ctx.free(dmem);
   TTB_TRY_END
 }
