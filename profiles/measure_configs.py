@@ -4,7 +4,8 @@
     python profiles/measure_configs.py            (on a B200; ~1 minute)
 
 Inputs: seeded N(0,1) cores generated on the device.  Timing: CUDA events on
-the current stream after one warm-up call, mean of `reps` calls.  B_alg and
+the current stream after three warm-up calls (pool growth, lazy module
+loading), mean of `reps` calls.  B_alg and
 F_alg are the SURVEY §8(d) algorithmic bytes / flops (paper_2011_06532_b200
 .cost, the reference's chain_estimate restated).
 """
@@ -33,8 +34,9 @@ def dev_random(comm, dims, ranks, seed):
     return T.DistTTTensor(comm, tuple(dims), tuple(ranks), slabs)
 
 
-def timed(fn, reps=5):
-    out = fn()
+def timed(fn, reps=5, warm=3):
+    for _ in range(warm):  # the stream-ordered pool and lazy module loading settle
+        out = fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -95,7 +97,7 @@ def main():
     # cfg5: X o W, d=12, n=50000, r=8 -> 64, round(max_rank=32, eps0=0)
     dims, r = (50_000,) * 12, (1,) + (8,) * 11 + (1,)
     x, w = dev_random(comm, dims, r, 0), dev_random(comm, dims, r, 1)
-    ms, p = timed(lambda: T.hadamard(x, w), reps=3)
+    ms, p = timed(lambda: T.hadamard(x, w), reps=3, warm=1)
     rows.append(("cfg5 hadamard", ms, core_bytes(dims, r) * 2 + core_bytes(dims, p.ranks), None))
     del x, w
     rounding("cfg5 round (cap 32)", p, T.RoundingOptions(0.0, "LRLI", max_rank=32), (1,) + (32,) * 11 + (1,))
