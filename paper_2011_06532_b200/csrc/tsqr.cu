@@ -25,7 +25,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // leaf kernel: one CTA = one chain of tiles over a contiguous slice run
 // ------------------------------------------------------------------------
 template <class C>
-__global__ void __launch_bounds__(C::NT, (C::NT <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(C::NT, C::MINB)
 tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __restrict__ Tg,
                  double* __restrict__ Rleaf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -734,10 +734,10 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   // pivot order) and the head tile always reaches b rows.
   const int64_t min_sl = std::max<int64_t>((b + rs - 1) / rs, 2 * (int64_t)f.plan.ni);
   int64_t gmax = ns >= min_sl ? ns / min_sl : 1;
-  // resident CTAs per SM: 2 for 256-thread leaf configurations, else 1
-  const int nt = f.cls == 16 ? Leaf16::NT : f.cls == 32 ? Leaf32::NT : Leaf64::NT;
+  // resident CTAs per SM of the leaf configuration (TCfg::MINB)
+  const int minb = f.cls == 16 ? Leaf16::MINB : f.cls == 32 ? Leaf32::MINB : Leaf64::MINB;
   static const int cps_env = getenv("TTB_LEAF_CPS") ? atoi(getenv("TTB_LEAF_CPS")) : 0;
-  const int cps = cps_env > 0 ? cps_env : (nt <= 256 ? 2 : 1);
+  const int cps = cps_env > 0 ? cps_env : minb;
   int G = (int)std::min<int64_t>((int64_t)cps * ctx.num_sms, std::max<int64_t>(1, gmax));
   if (ns == 0) G = 1;
   f.plan.G = G;

@@ -35,6 +35,8 @@ struct TCfg {
   static constexpr int NT = NW * 32;
   static constexpr int BMAX = NW * LC * CPL;
   static constexpr int MC = LR * RPL;
+  // resident CTAs per SM: two only when the register tile leaves room
+  static constexpr int MINB = (NT <= 256 && 2 * RPL * CPL + 64 <= 128) ? 2 : 1;
   static_assert(RPL % 2 == 0, "rows come in pairs (128-bit vector loads)");
   // tile row of register slot s in lane-row lr: consecutive pairs per lane
   __device__ __forceinline__ static int row(int s, int lr) { return (s >> 1) * (2 * LR) + 2 * lr + (s & 1); }
@@ -49,7 +51,7 @@ struct TCfg {
 // lane holds RPL rows x CPL columns of the register tile.
 // (TTB_LEAF64 etc. override a configuration at compile time for tuning runs)
 #ifndef TTB_LEAF64
-#define TTB_LEAF64 16, 2, 2, 16
+#define TTB_LEAF64 8, 2, 4, 16
 #endif
 #ifndef TTB_LEAF32
 #define TTB_LEAF32 8, 4, 1, 16
@@ -66,7 +68,7 @@ struct TCfg {
 #ifndef TTB_TREE16
 #define TTB_TREE16 8, 2, 1, 32
 #endif
-using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 512 threads, 1 CTA / SM
+using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 256 threads (4 columns each), 1 CTA / SM
 using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 128-row tiles
 using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 256-row tiles
 using Tree64 = TCfg<TTB_TREE64>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
