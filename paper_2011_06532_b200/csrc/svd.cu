@@ -20,10 +20,13 @@
 
 namespace ttb {
 
-constexpr int kSvdNT = 512;  // 256 threads on the A columns, 256 trailing on V
+#ifndef TTB_SVD_GRP
+#define TTB_SVD_GRP 16
+#endif
+constexpr int kGrp = TTB_SVD_GRP;  // threads per column pair
+constexpr int kSvdNT = 2 * 32 * kGrp;  // half on the A columns (one pair slot per group), half trailing on V
 constexpr int kSvdMax = 64;
 constexpr int kLd = kSvdMax + 1;  // padded column stride: distinct columns start on distinct banks
-constexpr int kGrp = 8;  // threads per column pair
 constexpr int kHalf = kSvdNT / 2;
 
 #ifdef TTB_DEBUG_CLK
