@@ -243,7 +243,7 @@ struct TreeHooks {
         double v = 0.0;
 #pragma unroll
         for (int s = 0; s < C::RPL; ++s)
-          if (s == sj) v = A[s][t];
+          if (C::pivot_slot(s) && s == sj) v = A[s][t];
         Rrow_out[(int64_t)j * ldr + k] = k >= j ? v : 0.0;
       }
     }

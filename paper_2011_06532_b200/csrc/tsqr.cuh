@@ -40,6 +40,9 @@ struct TCfg {
   static_assert(RPL % 2 == 0, "rows come in pairs (128-bit vector loads)");
   // tile row of register slot s in lane-row lr: consecutive pairs per lane
   __device__ __forceinline__ static int row(int s, int lr) { return (s >> 1) * (2 * LR) + 2 * lr + (s & 1); }
+  // head tiles: pivot rows are < BMAX; register slot s only holds rows >= (s/2)*2LR,
+  // so for slots with (s/2)*2LR >= BMAX every row-vs-pivot test is known at compile time
+  __host__ __device__ static constexpr bool pivot_slot(int s) { return (s >> 1) * 2 * LR < BMAX; }
   // owner of column j: warp j % NW, lane group (j / NW) % LC, slot j / (NW*LC)
   __device__ __forceinline__ static int owner_warp(int j) { return j % NW; }
   __device__ __forceinline__ static int owner_lc(int j) { return (j / NW) % LC; }
@@ -323,7 +326,7 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
 #pragma unroll
     for (int s = 0; s < RPL; s += 2) {
       double x0 = A[s][OT], x1 = A[s + 1][OT];
-      if (HEAD) {
+      if (HEAD && C::pivot_slot(s)) {
         x0 = C::row(s, lr) < j ? 0.0 : x0;
         x1 = C::row(s + 1, lr) < j ? 0.0 : x1;
       }
@@ -338,7 +341,7 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
 #pragma unroll
   for (int s = 0; s < RPL; ++s) {
     double x = A[s][OT];
-    if (HEAD) {
+    if (HEAD && C::pivot_slot(s)) {
       const int r = C::row(s, lr);
       if (r == j) aj = x;
       x = r > j ? x : 0.0;
@@ -370,7 +373,7 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
       const double x = A[s][OT];
-      if (HEAD) {  // rows > j: v = scal x (x_r for r > j); row j keeps R's beta
+      if (HEAD && C::pivot_slot(s)) {  // rows > j: v = scal x (x_r for r > j); row j keeps R's beta
         const int r = C::row(s, lr);
         A[s][OT] = r > j ? x * scal : (r == j ? beta : x);
       } else {
@@ -403,7 +406,7 @@ __device__ __forceinline__ void update_slot(double (&A)[C::RPL][C::CPL], const d
 #pragma unroll
     for (int s = 0; s < C::RPL; ++s) {
       double a = fma(-c, xr[s], A[s][T]);
-      if (HEAD && C::row(s, lr) == j) a = fma(c, beta, a);
+      if (HEAD && C::pivot_slot(s) && C::row(s, lr) == j) a = fma(c, beta, a);
       A[s][T] = a;
     }
     if (!HEAD && lr == 0) sm.Rs[j + C::BMAX * k] -= rcoef;
@@ -479,7 +482,7 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
 #pragma unroll
       for (int s = 0; s < RPL; ++s) {
         if (s & 1) a1 = fma(xr[s], A[s][t], a1); else a0 = fma(xr[s], A[s][t], a0);
-        if (HEAD && C::row(s, lr) == j) qa = A[s][t];
+        if (HEAD && C::pivot_slot(s) && C::row(s, lr) == j) qa = A[s][t];
       }
       p[t] = a0 + a1;
       q[t] = qa;
