@@ -88,6 +88,20 @@ int ttb_add(ttb_ctx* ctx, int nterms, int ndim, const int64_t* dims, const int64
 int ttb_hadamard(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
                  const double* const* x, const double* const* y, double* const* out);
 
+/* Seeded N(0,1) slabs, bitwise equal to the reference generator
+ * (fill_random_slab core.py:256-266, slice_rng core.py:250-253, used by
+ * random_tt core.py:269-282 and DistTTTensor.random parallel.py:88-102):
+ * slab s is core core[s]'s block of global slices [lo[s], lo[s] + dl[s]),
+ * shape (rl[s], dl[s], rr[s]) F-order, slice i drawn from
+ * Generator(Philox(SeedSequence(seed, spawn_key=(core[s], i)))).standard_normal.
+ * seed is the non-negative Python int as little-endian 32-bit words (0 -> one
+ * word 0; numpy's uint32 coercion).  Synchronizes the context stream (the
+ * rare ziggurat tail draws are finished with the host libm's log1p, as numpy
+ * does). */
+int ttb_fill_random(ttb_ctx* ctx, const uint32_t* seed, int nseed, int nslabs, const int64_t* core,
+                    const int64_t* lo, const int64_t* rl, const int64_t* dl, const int64_t* rr,
+                    double* const* out);
+
 /* ---- Gram sweeps ------------------------------------------------------ */
 /* <x, y> (ops.py:135-155): W_n = sum_i Y_n(i)^T W_{n-1} X_n(i), allreduced
  * per mode.  *result is written on the host. */

@@ -46,6 +46,8 @@ SIGNATURES = {
     "ttb_scale": (C.c_int, [_P, _I64, _P, C.c_double, _P]),
     "ttb_add": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PD, _PP]),
     "ttb_hadamard": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PP]),
+    "ttb_fill_random": (C.c_int, [_P, C.POINTER(C.c_uint32), C.c_int, C.c_int, _PI64, _PI64, _PI64, _PI64,
+                                  _PI64, _PP]),
     "ttb_inner": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PD]),
     "ttb_sumsq": (C.c_int, [_P, _I64, _P, _PD]),
     "ttb_orthonormalize": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PP]),

@@ -156,6 +156,41 @@ def random_tt(dims, ranks, seed: int) -> TTTensor:
     return TTTensor(cores)
 
 
+def seed_words(seed) -> list:
+    """A non-negative int seed as little-endian uint32 words, numpy's
+    SeedSequence entropy coercion (0 -> [0])."""
+    import operator
+
+    v = operator.index(seed)
+    if v < 0:
+        raise ValueError(f"expected non-negative integer seed, got {v}")
+    words = [v & 0xFFFFFFFF]
+    v >>= 32
+    while v:
+        words.append(v & 0xFFFFFFFF)
+        v >>= 32
+    return words
+
+
+def fill_random_slabs(comm, slabs, cores, lo, seed) -> None:
+    """Device form of fill_random_slab (core.py:256-266) for several slabs in
+    one call: slabs[k][:, j, :] <- stream of global slice lo[k] + j of core
+    cores[k].  Slabs must be F-order float64 on comm's device."""
+    import ctypes as C
+
+    from . import _lib
+
+    for t in slabs:
+        if not is_f_slab(t) or t.dtype.itemsize != 8 or not t.dtype.is_floating_point:
+            raise ShapeError("fill_random_slabs needs F-order float64 device slabs")
+    w = seed_words(seed)
+    lib = _lib.load()
+    _lib.check(lib.ttb_fill_random(
+        comm.ctx(), (C.c_uint32 * len(w))(*w), len(w), len(slabs), _lib.i64_array(cores), _lib.i64_array(lo),
+        _lib.i64_array([t.shape[0] for t in slabs]), _lib.i64_array([t.shape[1] for t in slabs]),
+        _lib.i64_array([t.shape[2] for t in slabs]), _lib.ptr_array([t.data_ptr() for t in slabs])))
+
+
 # ----------------------------------------------------------------------------
 # device slabs
 # ----------------------------------------------------------------------------
@@ -250,15 +285,16 @@ class DistTTTensor:
 
     @classmethod
     def random(cls, comm, dims, ranks, seed: int):
-        """This rank's slabs straight from the per-slice streams (parallel.py:88-102);
-        bitwise equal to distribute(random_tt(...)) for every P."""
+        """This rank's slabs straight from the per-slice streams (parallel.py:88-102),
+        generated on the device by ttb_fill_random: bitwise equal to
+        distribute(random_tt(...)) for every P."""
         dims, ranks = check_chain(dims, ranks)
-        slabs = []
+        slabs, lo = [], []
         for n, d in enumerate(dims):
-            lo, hi = block_bounds(d, comm.size, comm.rank)
-            arr = np.empty((ranks[n], hi - lo, ranks[n + 1]), order="F")
-            fill_random_slab(arr, n, lo, seed)
-            slabs.append(arr)
+            a, b = block_bounds(d, comm.size, comm.rank)
+            slabs.append(f_empty(ranks[n], b - a, ranks[n + 1], comm.device))
+            lo.append(a)
+        fill_random_slabs(comm, slabs, list(range(len(dims))), lo, seed)
         return cls(comm, dims, ranks, slabs)
 
     def copy(self):
