@@ -3,7 +3,7 @@
 
 Workload (BASELINE.json configs[2], the 2 GB-class tensor the metric and the
 north-star target are quoted on): Y random TT, d=10, n=8000 per mode,
-ranks 30, fp64 N(0,1) (seeded, generated on the device); X = Y + Y (ranks
+ranks 30, fp64 N(0,1) (the reference's random_tt seed 0, drawn on the device); X = Y + Y (ranks
 60, 1.85 GB of cores, built by our add kernel outside the timed region);
 one step = round_tt(X, RoundingOptions(1e-10, "LRLI")) -> ranks 30.
 
@@ -132,21 +132,11 @@ class Clocks:
 # our arm
 # ---------------------------------------------------------------------------
 def make_input(T, comm, cfg, seed=0):
-    """Device-generated Y (seeded N(0,1), this rank's slices) and X = Y + Y."""
-    import torch
-
-    from paper_2011_06532_b200.tensor import f_empty
-
+    """Y = the reference's random_tt(dims, ranks, seed) restricted to this
+    rank's slices, generated on the device bitwise equal to the host
+    generator (ttb_fill_random; core.py:250-282), and X = Y + Y."""
     dims, ry, _ = chain(cfg)
-    g = torch.Generator(device=comm.device)
-    slabs = []
-    for n, d in enumerate(dims):
-        lo, hi = T.block_bounds(d, comm.size, comm.rank)
-        g.manual_seed(seed * 1000003 + n * 1009 + comm.rank)
-        s = f_empty(ry[n], hi - lo, ry[n + 1], comm.device)
-        s.normal_(generator=g)
-        slabs.append(s)
-    y = T.DistTTTensor(comm, dims, ry, slabs)
+    y = T.DistTTTensor.random(comm, dims, ry, seed)
     return y, T.add(y, y)
 
 
@@ -297,7 +287,7 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded N(0,1) TT cores generated on device)",
+        "data": "synthetic: the reference generator's seeded N(0,1) cores (random_tt, seed 0), drawn on the device bitwise",
         "config": {"workload": f"{cfg}: round_tt(X = Y + Y) d={len(dims)} n={dims[0]} ranks {rx[1]}->{ry[1]}, "
                                f"tol {eps0}, LRLI", "dims": list(dims), "in_ranks": list(rx),
                    "out_ranks": list(ry), "parallelism": f"mode-sliced P={world}",

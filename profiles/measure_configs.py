@@ -3,7 +3,8 @@
 
     python profiles/measure_configs.py            (on a B200; ~1 minute)
 
-Inputs: seeded N(0,1) cores generated on the device.  Timing: CUDA events on
+Inputs: the reference's random_tt(dims, ranks, seed) cores, drawn on the
+device (bitwise equal to the host generator).  Timing: CUDA events on
 the current stream after three warm-up calls (pool growth, lazy module
 loading), mean of `reps` calls.  B_alg and
 F_alg are the SURVEY §8(d) algorithmic bytes / flops (paper_2011_06532_b200
@@ -20,18 +21,11 @@ sys.path.insert(0, ROOT)
 
 import paper_2011_06532_b200 as T  # noqa: E402
 from paper_2011_06532_b200 import cost  # noqa: E402
-from paper_2011_06532_b200.tensor import f_empty  # noqa: E402
 
 
 def dev_random(comm, dims, ranks, seed):
-    g = torch.Generator(device=comm.device)
-    g.manual_seed(seed)
-    slabs = []
-    for n, d in enumerate(dims):
-        s = f_empty(ranks[n], d, ranks[n + 1], comm.device)
-        s.normal_(generator=g)
-        slabs.append(s)
-    return T.DistTTTensor(comm, tuple(dims), tuple(ranks), slabs)
+    """The reference's random_tt(dims, ranks, seed), drawn on the device."""
+    return T.DistTTTensor.random(comm, dims, ranks, seed)
 
 
 def timed(fn, reps=5, warm=3):

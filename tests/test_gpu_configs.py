@@ -5,8 +5,8 @@ seconds, so they assert size-independent properties (rank recovery of an
 exactly low-rank sum, norm preservation under orthonormalization, the three
 norm routes agreeing, symmetry of the Gram sweep, the max_rank cap); the
 same shapes at reduced mode sizes are compared with the oracle directly.
-Inputs are seeded N(0,1) cores generated on the device (the full-size
-reference RNG on the host would take minutes; §8(f) row 1).
+Inputs are the reference's own seeded cores (random_tt(dims, ranks, seed)),
+drawn on the device bitwise equal to the host generator (§8(f) row 1).
 """
 import numpy as np
 import pytest
@@ -19,21 +19,13 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_2011_06532_b200 as T  # noqa: E402
 from oracle import tt_oracle as O  # noqa: E402
-from paper_2011_06532_b200.tensor import f_empty  # noqa: E402
 
 TOL_TT = 1e-10
 
 
 def dev_random(dims, ranks, seed):
-    comm = T.default_comm()
-    g = torch.Generator(device=comm.device)
-    g.manual_seed(seed)
-    slabs = []
-    for n, d in enumerate(dims):
-        s = f_empty(ranks[n], d, ranks[n + 1], comm.device)
-        s.normal_(generator=g)
-        slabs.append(s)
-    return T.DistTTTensor(comm, tuple(dims), tuple(ranks), slabs)
+    """The reference's random_tt(dims, ranks, seed), drawn on the device."""
+    return T.DistTTTensor.random(T.default_comm(), dims, ranks, seed)
 
 
 def dev(cores):
