@@ -158,6 +158,46 @@ int ttb_truncated_svd(ttb_ctx* ctx, int64_t m, int64_t n, const double* a, doubl
                       int64_t max_rank, double* u, double* s, double* v, int64_t* keep,
                       double* tail, int* capped);
 
+/* ---- Kronecker-operator apply (ops.py:238-342) ----------------------- */
+/* Mode-2 sparse product of one slab (mode2_multiply, core.py:285-297; the
+ * local product of _apply_term_dist, ops.py:309-311), written into the
+ * block (a0.., :, c0..) of an F-order output slab (out_rl, out_d, *):
+ *   out(a0+a, i, c0+c) = sum_{jj = indptr[i]}^{indptr[i+1]-1} vals[jj] * src(a, cols[jj], c)
+ * src(:, j, :) is local(:, j, :) for j < nloc (local: (rl, nloc, rr)
+ * F-order) and halo slice j - nloc otherwise (halo: slice-major, each slice
+ * an F-order rl x rr block -- the exchange payload layout, ops.py:284-287).
+ * indptr (nrows+1), cols, vals are DEVICE arrays (CSR, int64 indices).
+ * Accumulation is scipy's csr_matvecs sequence (bitwise). */
+int ttb_mode2_spmm(ttb_ctx* ctx, int64_t rl, int64_t rr, int64_t nrows, const int64_t* indptr,
+                   const int64_t* cols, const double* vals, int64_t nloc, const double* local,
+                   const double* halo, double* out, int64_t out_rl, int64_t out_d, int64_t a0,
+                   int64_t c0);
+/* out (slice-major, n slices of rl x rr F-order) = slab(:, idx[k], :) for
+ * the F-order slab (rl, I, rr); idx is a DEVICE int64 array.  Packs the
+ * payload of the operator exchange (ops.py:284-287). */
+int ttb_gather_slices(ttb_ctx* ctx, int64_t rl, int64_t I, int64_t rr, const double* slab, int64_t n,
+                      const int64_t* idx, double* out);
+/* Pairwise exchange with npeers peers in one NCCL group (replaces the
+ * round-robin comm.sendrecv rounds of ops.py:286-307): send[k] (send_n[k]
+ * doubles) goes to peers[k], recv[k] (recv_n[k] doubles) comes from it.
+ * Zero counts skip; both sides derive them from the replicated operator. */
+int ttb_exchange(ttb_ctx* ctx, int npeers, const int* peers, const double* const* send,
+                 const int64_t* send_n, double* const* recv, const int64_t* recv_n);
+
+/* ---- TT files (TTPAR1: save_tt / load_tt, core.py:364-398) ------------- */
+/* Read this rank's slice blocks [lo[n], hi[n]) of every core of a TTPAR1
+ * file into F-order device slabs out[n] (ranks[n], hi-lo, ranks[n+1]);
+ * data_offset = byte offset of core 0 (6 + 8 (2 ndim + 2)).  Staged through
+ * page-locked double buffers (host pread overlapped with H2D).  A short
+ * file raises TTB_ERR_SHAPE ("truncated"), as load_tt does.  Synchronous. */
+int ttb_read_slabs(ttb_ctx* ctx, const char* path, int64_t data_offset, int ndim, const int64_t* dims,
+                   const int64_t* ranks, const int64_t* lo, const int64_t* hi, double* const* out);
+/* Write this rank's slabs into an existing TTPAR1 file whose header is
+ * written and whose size is set (every rank writes only its own runs).
+ * Synchronous. */
+int ttb_write_slabs(ttb_ctx* ctx, const char* path, int64_t data_offset, int ndim, const int64_t* dims,
+                    const int64_t* ranks, const int64_t* lo, const int64_t* hi, const double* const* in);
+
 /* opt-in per-kernel-class timing with CUDA events (benchmark roofline);
  * dump writes "name launches total_ms\n" lines and clears the record. */
 int ttb_prof_enable(int on);

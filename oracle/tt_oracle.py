@@ -194,6 +194,59 @@ def hadamard(x, y, guard=None):
 
 
 # --------------------------------------------------------------------------
+# Kronecker operator apply (core.py:285-297, ops.py:265-342)
+# --------------------------------------------------------------------------
+
+def mode2_multiply(core, a):
+    """Y(i) = sum_j a[i, j] X(j): one sparse/dense product per right rank
+    (core.py:285-297)."""
+    rl, d, rr = core.shape
+    out = np.empty((rl, d, rr), order="F")
+    for r in range(rr):
+        out[:, :, r] = (a @ core[:, :, r].T).T
+    return out
+
+
+def apply_term_block(factor, core, lo, hi):
+    """Rows [lo, hi) of one term's mode-2 product as the distributed
+    reference computes them (ops.py:270-311): the factor's rows restricted to
+    the columns they touch, times the gathered source slices."""
+    import scipy.sparse as sp
+
+    a = sp.csr_matrix(factor)
+    rl, d, rr = core.shape
+    rows = a[lo:hi]
+    need = np.unique(rows.indices)
+    got = np.empty((need.size, rl * rr), order="F") if need.size else np.zeros((0, rl * rr))
+    for k, i in enumerate(need):
+        got[k] = core[:, int(i), :].ravel(order="F")
+    local = rows[:, need] @ got if need.size else np.zeros((hi - lo, rl * rr))
+    return np.asfortranarray(np.asarray(local).reshape(hi - lo, rr, rl).transpose(2, 0, 1))
+
+
+def apply_operator(terms, cores, round_eps=None, max_rank=None, nranks=1):
+    """Sum over terms of the per-core mode-2 products, TT-added left to
+    right, optionally rounded (ops.py:314-342).  nranks > 1 computes each
+    core as the concatenation of the distributed blocks."""
+    parts = []
+    for factors in terms:
+        if nranks == 1:
+            parts.append([mode2_multiply(c, a) for c, a in zip(cores, factors)])
+        else:
+            term = []
+            for c, a in zip(cores, factors):
+                blocks = [apply_term_block(a, c, *block_bounds(c.shape[1], nranks, p)) for p in range(nranks)]
+                term.append(np.asfortranarray(np.concatenate(blocks, axis=1)))
+            parts.append(term)
+    z = parts[0]
+    for extra in parts[1:]:
+        z = add(z, extra)
+    if round_eps is not None:
+        z, _ = round_tt(z, round_eps, "LRLI", max_rank)
+    return z
+
+
+# --------------------------------------------------------------------------
 # Gram sweeps (ops.py:135-235)
 # --------------------------------------------------------------------------
 

@@ -3,7 +3,8 @@
 Drop-in for the path-relevant public surface of the reference package
 ``ttpar`` (its __init__.py:10-95): TT construction, add / scale / hadamard,
 inner product and norms, left/right orthonormalization, truncated SVD,
-TSQR, and round_tt with RoundingOptions -- on device-resident,
+TSQR, round_tt with RoundingOptions, the
+Kronecker-operator apply and TTPAR1 files -- on device-resident,
 mode-sliced TT tensors, computed by hand-written sm_100a CUDA kernels
 (paper_2011_06532_b200/csrc, C ABI in include/ttb.h).
 """
@@ -11,19 +12,23 @@ mode-sliced TT tensors, computed by hand-written sm_100a CUDA kernels
 from .comm import Communicator, DistComm, SerialComm, default_comm
 from .errors import (BoundsError, CapabilityError, CapacityError, ContractError, DeadlockError,
                      NumericError, ShapeError, TTError)
+from .operator import KroneckerOperator, apply_operator, load_operator, mode2_multiply, save_operator
 from .ops import add, add_n, hadamard, inner_product, norm, scale
 from .parallel import (ROUNDING_VARIANTS, RoundingOptions, TruncatedSVD, TSQRFactor, distribute, gather,
                        orthonormalize, round_tt, round_tt_host, serial_tt, truncated_svd, tsqr_apply_q,
                        tsqr_factor)
 from .tensor import DistTTTensor, TTCore, TTTensor, block_bounds, random_tt
+from .ttio import load_tt, load_tt_dist, save_tt, save_tt_dist
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BoundsError", "CapabilityError", "CapacityError", "Communicator", "ContractError", "DeadlockError",
-    "DistComm", "DistTTTensor", "NumericError", "ROUNDING_VARIANTS", "RoundingOptions", "SerialComm",
+    "DistComm", "DistTTTensor", "KroneckerOperator", "NumericError", "ROUNDING_VARIANTS", "RoundingOptions", "SerialComm",
     "ShapeError", "TSQRFactor", "TTCore", "TTError", "TTTensor", "TruncatedSVD", "add", "add_n",
-    "block_bounds", "default_comm", "distribute", "gather", "hadamard", "inner_product", "norm",
-    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
+    "apply_operator", "block_bounds", "default_comm", "distribute", "gather", "hadamard", "inner_product", "load_operator",
+    "load_tt", "load_tt_dist", "mode2_multiply", "norm",
+    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "save_operator", "save_tt",
+    "save_tt_dist", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
     "tsqr_factor", "__version__",
 ]

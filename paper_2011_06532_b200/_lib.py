@@ -58,6 +58,11 @@ SIGNATURES = {
     "ttb_tsqr_free": (C.c_int, [_P, _P]),
     "ttb_truncated_svd": (C.c_int, [_P, _I64, _I64, _P, C.c_double, _I64, _P, _P, _P, _PI64, _PD,
                                     C.POINTER(C.c_int)]),
+    "ttb_mode2_spmm": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _I64, _I64]),
+    "ttb_gather_slices": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _P]),
+    "ttb_exchange": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _PP, _PI64, _PP, _PI64]),
+    "ttb_read_slabs": (C.c_int, [_P, C.c_char_p, _I64, C.c_int, _PI64, _PI64, _PI64, _PI64, _PP]),
+    "ttb_write_slabs": (C.c_int, [_P, C.c_char_p, _I64, C.c_int, _PI64, _PI64, _PI64, _PI64, _PP]),
     "ttb_fp64_peak": (C.c_int, [_P, _PD, _PD]),
     "ttb_prof_enable": (C.c_int, [C.c_int]),
     "ttb_prof_dump": (C.c_int, [C.c_char_p, C.c_longlong]),

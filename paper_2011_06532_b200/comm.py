@@ -68,6 +68,23 @@ class Communicator:
         except Exception:
             pass
 
+    # -- point-to-point exchange of device buffers ---------------------------
+    def exchange(self, peers, sends, recvs):
+        """Swap device buffers with peers in one grouped NCCL send/recv
+        (ttb_exchange): sends[k] (a float64 tensor or None) goes to
+        peers[k], recvs[k] (a float64 tensor view, possibly empty) is filled
+        from it.  Stream-ordered on the current stream."""
+        if not peers:
+            return
+        lib = _lib.load()
+        ctx = self.ctx()
+        sp = [0 if t is None else t.data_ptr() for t in sends]
+        sn = [0 if t is None else t.numel() for t in sends]
+        rp = [t.data_ptr() if t.numel() else 0 for t in recvs]
+        rn = [t.numel() for t in recvs]
+        _lib.check(lib.ttb_exchange(ctx, len(peers), (C.c_int * len(peers))(*peers), _lib.ptr_array(sp),
+                                    _lib.i64_array(sn), _lib.ptr_array(rp), _lib.i64_array(rn)))
+
     # -- host-side collectives (harness / gather) ----------------------------
     def allreduce_sum(self, arr):
         return np.asarray(arr, dtype=np.float64).copy()

@@ -24,6 +24,10 @@ struct NcclApi {
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
 };
 
 struct UniqueId { char internal[128]; };
@@ -50,6 +54,10 @@ static void load_nccl() {
   g_nccl.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclAllReduce");
   g_nccl.commDestroy = (int (*)(void*))dlsym(g_nccl.h, "ncclCommDestroy");
   g_nccl.getErrorString = (const char* (*)(int))dlsym(g_nccl.h, "ncclGetErrorString");
+  g_nccl.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclSend");
+  g_nccl.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclRecv");
+  g_nccl.groupStart = (int (*)())dlsym(g_nccl.h, "ncclGroupStart");
+  g_nccl.groupEnd = (int (*)())dlsym(g_nccl.h, "ncclGroupEnd");
   TTB_CHECK(g_nccl.getUniqueId && g_commInitRank && g_nccl.allGather && g_nccl.allReduce, TTB_ERR_NCCL,
             "libnccl is missing required symbols");
 }
@@ -119,6 +127,22 @@ void Ctx::allgather(const double* send, double* recv, size_t count) {
 void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
   nccl_check(g_nccl.allReduce(send, recv, count, kNcclDouble, kNcclSum, nccl_comm, stream), "ncclAllReduce");
+}
+
+void Ctx::sendrecv(int npeers, const int* peers, const double* const* send, const int64_t* send_n,
+                   double* const* recv, const int64_t* recv_n) {
+  if (npeers == 0) return;
+  TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
+  TTB_CHECK(g_nccl.send && g_nccl.recv && g_nccl.groupStart && g_nccl.groupEnd, TTB_ERR_NCCL,
+            "libnccl lacks ncclSend/ncclRecv");
+  nccl_check(g_nccl.groupStart(), "ncclGroupStart");
+  for (int k = 0; k < npeers; ++k) {
+    if (send_n[k] > 0) nccl_check(g_nccl.send(send[k], (size_t)send_n[k], kNcclDouble, peers[k], nccl_comm, stream),
+                                  "ncclSend");
+    if (recv_n[k] > 0) nccl_check(g_nccl.recv(recv[k], (size_t)recv_n[k], kNcclDouble, peers[k], nccl_comm, stream),
+                                  "ncclRecv");
+  }
+  nccl_check(g_nccl.groupEnd(), "ncclGroupEnd");
 }
 
 void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }

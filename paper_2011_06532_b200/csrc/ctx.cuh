@@ -50,6 +50,9 @@ struct Ctx {
   // collectives on this->stream (nranks > 1 only)
   void allgather(const double* send, double* recv, size_t count);
   void allreduce_sum(const double* send, double* recv, size_t count);
+  // grouped point-to-point exchange with a set of peers (zero counts skip)
+  void sendrecv(int npeers, const int* peers, const double* const* send, const int64_t* send_n,
+                double* const* recv, const int64_t* recv_n);
   void sync();
 };
 

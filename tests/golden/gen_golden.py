@@ -120,6 +120,60 @@ def main():
     put_dt("cfg1s_out", out)
     g["cfg1s_norm"] = np.array(out.meta["norm"])
 
+    # 9. Kronecker operator apply (ops.py:238-342) and mode-2 products
+    import tempfile
+
+    import scipy.sparse as sp
+    from ttpar import (KroneckerOperator, apply_operator, load_tt, mode2_multiply,
+                       save_operator, save_tt, distribute)
+
+    def lap(d):
+        return sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(d, d), format="csr")
+
+    def kron_sum(dims):
+        terms = []
+        for n in range(len(dims)):
+            row = [sp.identity(d, format="csr") for d in dims]
+            row[n] = lap(dims[n])
+            terms.append(row)
+        return KroneckerOperator(dims, terms)
+
+    rng = np.random.default_rng(31)
+    m2_core = rng.standard_normal((3, 9, 4))
+    m2_a = sp.random(9, 9, density=0.4, random_state=5, format="csr")
+    g["m2_core"] = np.asfortranarray(m2_core)
+    g["m2_a_dense"] = m2_a.toarray()
+    g["m2_out"] = mode2_multiply(ttpar.TTCore(m2_core), m2_a).array
+    op_dims = (6, 5, 7)
+    ox = random_tt(op_dims, (1, 3, 4, 1), seed=27)
+    put_tt("op_x", ox)
+    op = kron_sum(op_dims)
+    put_tt("op_lap", apply_operator(op, ox))
+    put_tt("op_lap_round", apply_operator(op, ox, round_eps=1e-10))
+    for p in (2, 3):
+        res = run_spmd(p, lambda comm: gather(apply_operator(op, distribute(ox, comm))))
+        put_tt(f"op_lap_p{p}", res.results[0])
+    # cyclic shift + identity (test_acceptance.py:69-75)
+    eye = [sp.identity(d, format="csr") for d in op_dims]
+    shifted = [sp.csr_matrix((np.ones(d), (np.arange(d), (np.arange(d) + 1) % d)), shape=(d, d))
+               for d in op_dims]
+    put_tt("op_shift", apply_operator(KroneckerOperator(op_dims, [eye, shifted]), ox))
+    # single mode: the terms sum elementwise
+    o1 = random_tt((8,), (1, 1), seed=3)
+    put_tt("op1_x", o1)
+    put_tt("op1_lap", apply_operator(KroneckerOperator((8,), [[lap(8)], [sp.identity(8, format="csr")]]), o1))
+
+    # 10. files: TTPAR1 bytes (core.py:364-372) and KRONOP1 text (ops.py:345-357)
+    with tempfile.TemporaryDirectory() as td:
+        ft = random_tt((5, 4, 3), (1, 2, 3, 1), seed=12)
+        put_tt("file_tt", ft)
+        save_tt(os.path.join(td, "t.tt"), ft)
+        g["file_tt_bytes"] = np.frombuffer(open(os.path.join(td, "t.tt"), "rb").read(), dtype=np.uint8)
+        assert all(np.array_equal(a.array, b.array)
+                   for a, b in zip(load_tt(os.path.join(td, "t.tt")).cores, ft.cores))
+        save_operator(os.path.join(td, "op.kron"), kron_sum((4, 3, 5)))
+        g["file_op_bytes"] = np.frombuffer(open(os.path.join(td, "op.kron"), "rb").read(), dtype=np.uint8)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 
