@@ -16,6 +16,24 @@ namespace ttb {
 constexpr int kEwNT = 256;
 constexpr int kEwElems = 4096;  // target output elements per CTA
 
+// Visit the cells (row r, slice ii) of an RL x nn block of an F-order core
+// column, rows fastest so stores coalesce.  mk(r) returns the per-row
+// functor g(ii); row-dependent index arithmetic (divisions) runs once per
+// thread when RL <= the CTA size instead of once per element.
+template <class MK>
+__device__ __forceinline__ void for_cells(int RL, int nn, MK&& mk) {
+  if (RL <= kEwNT) {
+    const int per = kEwNT / RL;
+    const int r = threadIdx.x % RL, i0 = threadIdx.x / RL;
+    if (i0 >= per) return;
+    auto g = mk(r);
+    for (int ii = i0; ii < nn; ii += per) g(ii);
+  } else {
+    for (int ii = 0; ii < nn; ++ii)
+      for (int r = threadIdx.x; r < RL; r += kEwNT) mk(r)(ii);
+  }
+}
+
 struct AddArgs {
   int mode;  // 0 interior (block diagonal), 1 first core (concat along c), 2 last core (stack along a), 3 single core (sum)
   int nterms;
@@ -53,23 +71,25 @@ __global__ void __launch_bounds__(kEwNT) add_kernel(AddArgs a) {
     return;
   }
   if (a.mode == 2) {  // RR == 1: out(a, i, 0) = X_p(a - offa, i, 0)
-    for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
-      const int64_t ai = e % RL, ii = e / RL;
+    for_cells((int)RL, (int)ni, [&](int ai) {
       int p = 0;
       for (int q = 0; q < a.nterms; ++q)
         if (ai >= a.t[q].offa) p = q;
-      const AddTerm& U = a.t[p];
-      out[e] = U.x[(ai - U.offa) + U.rl * (i0 + ii)];
-    }
+      const double* x = a.t[p].x + (ai - a.t[p].offa) + a.t[p].rl * i0;
+      const int64_t rl = a.t[p].rl;
+      return [=](int ii) { out[ai + RL * ii] = x[rl * ii]; };
+    });
     return;
   }
   // interior: block diagonal
   const double* x = T.x + T.rl * (i0 + a.I * (c - T.offc));
-  for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
-    const int64_t ai = e % RL, ii = e / RL;
+  for_cells((int)RL, (int)ni, [&](int ai) {
     const int64_t al = ai - T.offa;
-    out[e] = (al >= 0 && al < T.rl) ? x[al + T.rl * ii] : 0.0;
-  }
+    const bool in = al >= 0 && al < T.rl;
+    const double* xr = x + al;
+    const int64_t rl = T.rl;
+    return [=](int ii) { out[ai + RL * ii] = in ? xr[rl * ii] : 0.0; };
+  });
 }
 
 void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, int64_t I, int64_t RR, double* out) {
@@ -100,22 +120,23 @@ hadamard_kernel(const double* __restrict__ x, int64_t ral, int64_t rar, const do
   const int64_t RL = ral * rbl;
   const int64_t i0 = (int64_t)blockIdx.x * ni;
   const int64_t nn = min64(ni, I - i0);
-  const int64_t cnt = RL * nn;
   double* o = out + RL * (i0 + I * col);
   const double* xs = x + ral * (i0 + I * bx);
   const double* ys = y + rbl * (i0 + I * dy);
-  for (int64_t e = threadIdx.x; e < cnt; e += kEwNT) {
-    const int64_t row = e % RL, ii = e / RL;
-    const int64_t ax = row / rbl, cy = row - ax * rbl;
-    o[e] = __dmul_rn(xs[ax + ral * ii], ys[cy + rbl * ii]);
-  }
+  for_cells((int)RL, (int)nn, [&](int row) {
+    const int ax = row / (int)rbl, cy = row - ax * (int)rbl;
+    const double* xp = xs + ax;
+    const double* yp = ys + cy;
+    double* op = o + row;
+    return [=](int ii) { op[RL * ii] = __dmul_rn(xp[ral * ii], yp[rbl * ii]); };
+  });
 }
 
 void hadamard_core(Ctx& ctx, const double* x, int64_t ral, int64_t rar, const double* y, int64_t rbl, int64_t rbr,
                    int64_t I, double* out) {
   const int64_t RL = ral * rbl, RR = rar * rbr;
   if (I == 0) return;
-  TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "hadamard: output right rank too large");
+  TTB_CHECK(RR <= 65535 && RL <= (1 << 24), TTB_ERR_CAPABILITY, "hadamard: output rank too large");
   int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
   dim3 grid((unsigned)((I + ni - 1) / ni), (unsigned)RR);
   ProfScope ps("hadamard", ctx.stream);

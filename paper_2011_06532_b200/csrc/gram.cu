@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(NT, 1) gram2_kernel(Gram2Args a) {
   const bool bactive = bt < nbt;
   const int b = bt * 8 + fr;                // this lane's b in A fragments of X^T
   const int nct = (rbl + 7) / 8, ndt = (rbr + 7) / 8;
-  constexpr int U = 2;  // slices in flight per warp (independent accumulator chains)
+#ifndef TTB_GRAM_U
+#define TTB_GRAM_U 2
+#endif
+  constexpr int U = TTB_GRAM_U;  // slices in flight per warp (independent accumulator chains)
   double acc[U][kG2MaxD][2];
 #pragma unroll
   for (int u = 0; u < U; ++u)

@@ -31,22 +31,31 @@ mode2_spmm_kernel(int64_t rl, int64_t rr, int64_t nrows, const int64_t* __restri
                   int64_t out_rl, int64_t out_d, int64_t a0, int64_t c0, int ni) {
   const int64_t c = blockIdx.y;
   const int64_t i0 = (int64_t)blockIdx.x * ni;
-  const int64_t cnt = rl * min64(ni, nrows - i0);
+  const int nn = (int)min64(ni, nrows - i0);
   const double* loc = local + rl * nloc * c;
   const double* hal = halo + rl * c;
   const int64_t hstride = rl * rr;
-  double* o = out + a0 + out_rl * (out_d * (c0 + c));
-  for (int64_t e = threadIdx.x; e < cnt; e += kSpNT) {
-    const int64_t a = e % rl;
-    const int64_t i = i0 + e / rl;
-    const int64_t beg = indptr[i], end = indptr[i + 1];
+  double* o = out + a0 + out_rl * (i0 + out_d * (c0 + c));
+  const int64_t* ip = indptr + i0;
+  // rows a fastest (coalesced stores); per-thread row fixed when rl <= CTA size
+  auto cell = [&](int a, int ii) {
+    const int64_t beg = ip[ii], end = ip[ii + 1];
     double acc = 0.0;
     for (int64_t jj = beg; jj < end; ++jj) {
       const int64_t j = cols[jj];
       const double x = j < nloc ? loc[a + rl * j] : hal[a + hstride * (j - nloc)];
       acc = __dadd_rn(acc, __dmul_rn(vals[jj], x));
     }
-    o[a + out_rl * i] = acc;
+    o[a + out_rl * ii] = acc;
+  };
+  if (rl <= kSpNT) {
+    const int per = kSpNT / (int)rl;
+    const int a = threadIdx.x % (int)rl, g = threadIdx.x / (int)rl;
+    if (g < per)
+      for (int ii = g; ii < nn; ii += per) cell(a, ii);
+  } else {
+    for (int ii = 0; ii < nn; ++ii)
+      for (int a = threadIdx.x; a < rl; a += kSpNT) cell(a, ii);
   }
 }
 
