@@ -65,6 +65,10 @@ long long ttb_launch_counter(void);
 int ttb_ctx_create(int device, void* stream, ttb_ctx** out);
 int ttb_ctx_destroy(ttb_ctx* ctx);
 int ttb_ctx_set_stream(ttb_ctx* ctx, void* stream);
+/* Return the device memory the library's stream-ordered pool keeps cached
+ * (workspace is kept mapped between calls for speed) to the driver, after
+ * the context's streams drained.  The analogue of torch.cuda.empty_cache(). */
+int ttb_ctx_trim(ttb_ctx* ctx);
 /* NCCL bootstrap: rank 0 creates the id, the host broadcasts it
  * (replaces MPICommunicator, comm.py:359-401). */
 int ttb_comm_unique_id(void* out128);

@@ -41,6 +41,7 @@ SIGNATURES = {
     "ttb_ctx_create": (C.c_int, [C.c_int, _P, _PP]),
     "ttb_ctx_destroy": (C.c_int, [_P]),
     "ttb_ctx_set_stream": (C.c_int, [_P, _P]),
+    "ttb_ctx_trim": (C.c_int, [_P]),
     "ttb_comm_unique_id": (C.c_int, [_P]),
     "ttb_ctx_init_comm": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "ttb_scale": (C.c_int, [_P, _I64, _P, C.c_double, _P]),

@@ -57,6 +57,12 @@ class Communicator:
     def _init_comm(self):
         _lib.check(_lib.load().ttb_ctx_init_comm(self._ctx, 1, 0, None))
 
+    def empty_cache(self):
+        """Hand the library's cached device workspace back to the driver
+        (ttb_ctx_trim; the analogue of torch.cuda.empty_cache())."""
+        if self._ctx is not None:
+            _lib.check(_lib.load().ttb_ctx_trim(self._ctx))
+
     def close(self):
         if self._ctx is not None:
             _lib.load().ttb_ctx_destroy(self._ctx)
@@ -195,6 +201,12 @@ class _NullTrace:
 
 
 _default = {}
+
+
+def empty_cache():
+    """Release the cached device workspace of every default communicator."""
+    for comm in _default.values():
+        comm.empty_cache()
 
 
 def default_comm():

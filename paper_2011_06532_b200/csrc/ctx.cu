@@ -254,6 +254,19 @@ int ttb_ctx_set_stream(ttb_ctx* ctx, void* stream) {
   TTB_TRY_END
 }
 
+int ttb_ctx_trim(ttb_ctx* ctx) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(ctx, TTB_ERR_CONTRACT, "null context");
+  TTB_CUDA(cudaSetDevice(ctx->c.device));
+  ctx->c.collect(true);
+  TTB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  if (ctx->c.side) TTB_CUDA(cudaStreamSynchronize(ctx->c.side));
+  cudaMemPool_t pool;
+  TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
+  TTB_CUDA(cudaMemPoolTrimTo(pool, 0));
+  TTB_TRY_END
+}
+
 int ttb_comm_unique_id(void* out128) {
   TTB_TRY_BEGIN
   load_nccl();

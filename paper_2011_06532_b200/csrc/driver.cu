@@ -220,7 +220,7 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
       tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 0), f);
       double* eye = make_eye(ctx, b);
       tsqr_apply(ctx, f, eye, b, panel_of(out[n], ranks[n], dims[n], b, 0));
-      gemm_small_left(ctx, b, b, dims[n + 1] * ranks[n + 2], f.R, b, false, in[n + 1], out[n + 1]);
+      gemm_small_left(ctx, b, b, dims[n + 1] * ranks[n + 2], f.R, b, false, in[n + 1], out[n + 1], true);
       ctx.free(eye);
       tsqr_release(ctx, f);
       work = out[n + 1];
@@ -233,7 +233,7 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
       tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 1), f);
       double* eye = make_eye(ctx, b);
       tsqr_apply(ctx, f, eye, b, panel_of(out[n], b, dims[n], ranks[n + 1], 1));
-      gemm_small_right(ctx, ranks[n - 1] * dims[n - 1], b, b, in[n - 1], f.R, b, true, out[n - 1]);
+      gemm_small_right(ctx, ranks[n - 1] * dims[n - 1], b, b, in[n - 1], f.R, b, true, out[n - 1], true);
       ctx.free(eye);
       tsqr_release(ctx, f);
       work = out[n - 1];
@@ -386,7 +386,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], r[n], d[n], b, 0));
         ctx.free(eye);
       }
-      gemm_small_left(ctx, b, b, d[n + 1] * r[n + 2], facs[n].R, b, false, in[n + 1], out[n + 1]);
+      gemm_small_left(ctx, b, b, d[n + 1] * r[n + 2], facs[n].R, b, false, in[n + 1], out[n + 1], true);
       if (!implicit) tsqr_release(ctx, facs[n]);
     }
     last = out[N - 1];
@@ -403,7 +403,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], b, d[n], r[n + 1], 1));
         ctx.free(eye);
       }
-      gemm_small_right(ctx, r[n - 1] * d[n - 1], b, b, in[n - 1], facs[n].R, b, true, out[n - 1]);
+      gemm_small_right(ctx, r[n - 1] * d[n - 1], b, b, in[n - 1], facs[n].R, b, true, out[n - 1], true);
       if (!implicit) tsqr_release(ctx, facs[n]);
     }
     last = out[0];

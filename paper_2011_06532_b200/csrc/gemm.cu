@@ -30,6 +30,7 @@ struct SkinnyArgs {
   int64_t bsk, bsj;
   double* O;          // out(m, j) = O[m * osm + j * osj]
   int64_t osm, osj;
+  int upper;          // S is upper triangular (S(m, k) = 0 for k < m): the R-folds (dtrmm)
 };
 
 template <int MB>  // M rounded up to MB*8
@@ -63,7 +64,10 @@ __global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
     for (int q = 0; q < kSkMaxK / 4; ++q) {
       if (4 * q >= KP) break;
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) dmma_884(acc[mb][0], acc[mb][1], Ss[(mb * 8 + ar) * LDS + 4 * q + ac], bf[q]);
+      for (int mb = 0; mb < MB; ++mb) {
+        if (a.upper && 4 * q + 4 <= mb * 8) continue;  // all-zero block of a triangular S
+        dmma_884(acc[mb][0], acc[mb][1], Ss[(mb * 8 + ar) * LDS + 4 * q + ac], bf[q]);
+      }
     }
     // D fragment: row mb*8 + lane/4, columns j0 + 2*(lane%4) + {0, 1}
     const int orow = lane >> 2, ocol = 2 * (lane & 3);
@@ -102,13 +106,23 @@ static void launch_skinny(Ctx& ctx, const SkinnyArgs& a) {
 // contiguous block, one bulk copy (TMA engine) each, kFoldStages - 1 chunks
 // in flight -- and multiplied by the small operand held in shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kFoldJ = 64;
-constexpr int kFoldStages = 5;
+#ifndef TTB_FOLD_J
+#define TTB_FOLD_J 64
+#endif
+#ifndef TTB_FOLD_STAGES
+#define TTB_FOLD_STAGES 2
+#endif
+#ifndef TTB_FOLD_MINB
+#define TTB_FOLD_MINB 2
+#endif
+constexpr int kFoldJ = TTB_FOLD_J;
+constexpr int kFoldStages = TTB_FOLD_STAGES;
 constexpr int kFoldNT = 256;
+constexpr int kFoldMinB = TTB_FOLD_MINB;  // resident CTAs per SM
 
 __device__ __forceinline__ unsigned fd_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(kFoldNT, 1) fold_left_kernel(SkinnyArgs a) {
+__global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArgs a) {
   extern __shared__ __align__(128) double fsm[];
   constexpr int NW = kFoldNT / 32;
   const int M = a.M, K = a.K;
@@ -169,8 +183,9 @@ __global__ void __launch_bounds__(kFoldNT, 1) fold_left_kernel(SkinnyArgs a) {
       const double* b1p = bs + (int64_t)K * (n0 + 8 + fr);
       const double* a0p = Ss + (int64_t)(m0 + fr) * ldS;
       const double* a1p = Ss + (int64_t)(m0 + 8 + fr) * ldS;
+      // upper-triangular S (the R-fold, dtrmm): rows m0.. have no entries left of column m0
 #pragma unroll 4
-      for (int k0 = 0; k0 < KP; k0 += 4) {
+      for (int k0 = a.upper ? m0 : 0; k0 < KP; k0 += 4) {
         const int k = k0 + fc;
         const bool kin = k < K;
         const double a0 = a0p[k], a1 = a1p[k];  // zero padded
@@ -206,7 +221,7 @@ __global__ void __launch_bounds__(kFoldNT, 1) fold_left_kernel(SkinnyArgs a) {
 
 static bool fold_left_tma(Ctx& ctx, const SkinnyArgs& a) {
   // bulk copies need 16-byte sizes / addresses: K * columns even, aligned base
-  if (a.K % 2 != 0 || ((uintptr_t)a.B & 15) || a.N < (int64_t)kFoldJ * ctx.num_sms) return false;
+  if (a.K % 2 != 0 || ((uintptr_t)a.B & 15) || a.N < (int64_t)kFoldJ * ctx.num_sms) return false;  // (enough chunks for every SM)
   const int ldS = ((a.K + 11) & ~15) + 4, MP = (a.M + 15) & ~15;
   const size_t smem = (16 + (size_t)MP * ldS + 16 + (size_t)kFoldStages * a.K * kFoldJ) * sizeof(double);
   static bool attr = false;
@@ -214,9 +229,9 @@ static bool fold_left_tma(Ctx& ctx, const SkinnyArgs& a) {
     TTB_CUDA(cudaFuncSetAttribute(fold_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  if (smem > 227 * 1024) return false;
+  if (smem * kFoldMinB > 227 * 1024) return false;
   const int64_t nch = (a.N + kFoldJ - 1) / kFoldJ;
-  const int grid = (int)std::min<int64_t>(nch, ctx.num_sms);
+  const int grid = (int)std::min<int64_t>(nch, (int64_t)kFoldMinB * ctx.num_sms);
   fold_left_kernel<<<grid, kFoldNT, smem, ctx.stream>>>(a);
   TTB_LAUNCHED();
   return true;
@@ -224,7 +239,7 @@ static bool fold_left_tma(Ctx& ctx, const SkinnyArgs& a) {
 
 // out_H (M x N) = F (M x K) * H (K x N); H col-major ld K, out col-major ld M
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
-                     double* out) {
+                     double* out, bool upper) {
   ProfScope ps("fold_left", ctx.stream);
   SkinnyArgs a;
   a.M = M;
@@ -239,13 +254,14 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
   a.O = out;
   a.osm = 1;
   a.osj = M;
+  a.upper = upper ? 1 : 0;
   if (getenv("TTB_FOLD_V1") == nullptr && fold_left_tma(ctx, a)) return;
   launch_skinny(ctx, a);
 }
 
 // out_V (Mb x Nn) = V (Mb x K) * G (K x Nn): computed as out^T = G^T V^T
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
-                      double* out) {
+                      double* out, bool upper) {
   ProfScope ps("fold_right", ctx.stream);
   SkinnyArgs a;
   a.M = Nn;
@@ -260,6 +276,7 @@ void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, cons
   a.O = out;  // out(c, r) = out_V(r, c) = out[r + Mb*c]
   a.osm = Mb;
   a.osj = 1;
+  a.upper = upper ? 1 : 0;  // S = G^T: upper triangular when G is lower (V R^T)
   launch_skinny(ctx, a);
 }
 

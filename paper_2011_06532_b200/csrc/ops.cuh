@@ -26,10 +26,12 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
 
 // gemm.cu: skinny products on unfoldings
 // out_H (M x N) = F (M x K) * H (K x N); col-major, ldH = K, ldOut = M, F ld = ldf (F^T if transF)
+// upper: F is upper triangular (the R-fold, dtrmm) -- zero blocks are skipped
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
-                     double* out);
+                     double* out, bool upper = false);
 // out_V (Mb x Nn) = V (Mb x K) * G (K x Nn); col-major, ldV = Mb, ldOut = Mb, G ld = ldg (G^T if transG)
+// upper: the effective small operand S(c, k) = G(k, c) is upper triangular (V R^T: transG, G = R)
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
-                      double* out);
+                      double* out, bool upper = false);
 
 }  // namespace ttb

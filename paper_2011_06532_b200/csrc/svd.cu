@@ -45,6 +45,7 @@ struct SvdSmem {
   int order[kSvdMax];
   int rotated;
   int bad;
+  unsigned long long maxoff;  // max over the sweep of ga^2 / (al be) (a non-negative double's bits)
 };
 
 // reduction over the 8 lanes of one pair group (every lane of the warp
@@ -120,7 +121,10 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
         if ((ltid % 32) == 0) sm.nrm[c] = acc;
       }
     }
-    if (tid == 0) sm.rotated = 0;
+    if (tid == 0) {
+      sm.rotated = 0;
+      sm.maxoff = 0ull;
+    }
     __syncthreads();
     double nmax = 0.0;
     for (int c = 0; c < n; ++c) nmax = fmax(nmax, sm.nrm[c]);
@@ -180,6 +184,9 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
               sm.nrm[p] = fma(-t, ga, al);
               sm.nrm[q] = fma(t, ga, be);
               sm.rotated = 1;
+#ifndef TTB_SVD_NO_EARLY_STOP
+              atomicMax(&sm.maxoff, (unsigned long long)__double_as_longlong(ga * ga / (al * be)));
+#endif
             }
           }
           if (live && gl == 0) {
@@ -212,9 +219,17 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
       __syncthreads();
     }
     const int any = sm.rotated;
+    // quadratic convergence: once every rotation of a sweep had
+    // |cos angle(a_p, a_q)| < 1e-9, the next sweep's rotations are of order
+    // 1e-18 -- below the rotation threshold tol ~ 1e-14 -- so that sweep
+    // would only confirm convergence; skip it
+    const double maxoff = __longlong_as_double((long long)sm.maxoff);
     __syncthreads();
     ++sweeps;
     if (!any) break;
+#ifndef TTB_SVD_NO_EARLY_STOP
+    if (maxoff < 1e-18) break;
+#endif
   }
   // singular values
   for (int c = tid / 32; c < n; c += kSvdNT / 32) {

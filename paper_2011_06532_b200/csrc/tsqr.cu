@@ -61,7 +61,7 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     const bool head = (t == 0);
     tile_qr<C>(A, b, head, sm, t * b);
     const int64_t tile = tb + t;
-    store_Y<C>(A, b, head, Yg + tile * (int64_t)C::MC * b, C::MC);
+    store_Y_units<C>(A, b, head, Yg + tile * y_tile_stride(C::MC, b));
     store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
     if (head) extract_R<C>(A, b, sm);
     __syncthreads();
@@ -475,9 +475,9 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_chain_kernel(ChainArgs a) {
     auto Ta = [&](int m, int l) { return (l >= m && l < b && m < b) ? Tc[m + b * l] : 0.0; };
     if (t == 0) {
       // head: u_0 = T_0 (V_top^T z_0), V_top = rows 0..b-1 of Y_0 (global)
-      const double* Y0 = a.Y + tb * (int64_t)a.ldy * b;
+      const double* Y0 = a.Y + tb * y_tile_stride(a.ldy, b);  // rows < b: unit 0
       cta_dmma(
-          b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Y0[l + (int64_t)a.ldy * m] : 0.0; },
+          b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Y0[l + (int64_t)kYLd * m] : 0.0; },
           [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
           [&](int m, int n, double v) { W[m + ld * n] = v; });
       __syncthreads();
@@ -524,10 +524,9 @@ struct ProductArgs {
 // i+1's rows of Y_t and its u_t stream into shared memory while unit i is
 // multiplied.
 constexpr int kProdStages = 2;
-constexpr int kProdRows = 128;  // unit rows when a whole tile does not fit two stages
 
 struct ProductUnit {
-  int rows;  // rows per work unit: the tile (ldy) or kProdRows
+  int rows;  // rows per work unit (kYUnit)
   __host__ __device__ static size_t smem(int ur, int b, int k) {
     return 128 + (size_t)kProdStages * ((size_t)(ur + 4) * b + (size_t)b * ldpad(k)) * sizeof(double);
   }
@@ -553,8 +552,8 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
   constexpr int NW = kProdNT / 32;
   const LeafPlan& pl = a.plan;
   const int b = pl.b, k = a.k, ldy = a.ldy, rs = pl.rs, ni = pl.ni;
-  const int UR = a.unit_rows;
-  const int lys = UR + 4;  // = ldpad(UR) for UR a multiple of 16
+  const int UR = kYUnit;
+  const int lys = kYLd;
   const int ldu = ldpad(k);
   const int halves = ldy / UR;
   const int64_t nunits = pl.total_tiles() * halves;
@@ -573,12 +572,14 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
     if (threadIdx.x >= 32) return;
     const int64_t tile = unit / halves;
     const int r0 = (int)(unit - tile * halves) * UR;
-    if (threadIdx.x == 0) mbar_expect_tx(&bar[st], (unsigned)(UR * b * 8) + ubytes);
+    if (threadIdx.x == 0) mbar_expect_tx(&bar[st], (unsigned)(ystage * 8) + ubytes);
     __syncwarp();
-    const double* Yg = a.Y + tile * (int64_t)ldy * b + r0;
-    for (int j = threadIdx.x; j < b; j += 32)
-      bulk_g2s(Ysb + st * ystage + (int64_t)lys * j, Yg + (int64_t)ldy * j, UR * 8, &bar[st]);
-    if (threadIdx.x == 0) bulk_g2s(Usb + st * ustage, a.u + tile * ustage, ubytes, &bar[st]);
+    // the unit is one contiguous block (unit-major Y layout)
+    const double* Yg = a.Y + tile * y_tile_stride(ldy, b) + (int64_t)(r0 / kYUnit) * b * kYLd;
+    if (threadIdx.x == 0) {
+      bulk_g2s(Ysb + st * ystage, Yg, (unsigned)(ystage * 8), &bar[st]);
+      bulk_g2s(Usb + st * ustage, a.u + tile * ustage, ubytes, &bar[st]);
+    }
   };
   int64_t unit = blockIdx.x;
   if (unit < nunits) issue(unit, 0);
@@ -766,7 +767,7 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   size_t total = 0;
   auto add = [&](int64_t cnt) { size_t off = total; total += ((size_t)cnt * 8 + 255) / 256 * 256; return off; };
   const int64_t tsz = (bb + 1) & ~1LL;
-  size_t oY = add(ntiles * MC * b), oT = add(ntiles * tsz), oRl = add((int64_t)G * bb);
+  size_t oY = add(ntiles * y_tile_stride(MC, b)), oT = add(ntiles * tsz), oRl = add((int64_t)G * bb);
   size_t oLY[kMaxLevels], oLT[kMaxLevels], oLR[kMaxLevels];
   for (int L = 0; L < f.nloc; ++L) {
     oLY[L] = add((int64_t)nodes_loc[L] * MT * b);
@@ -883,8 +884,8 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.z0 = z0buf;
   pa.k = k;
   pa.out = out;
-  TTB_CHECK(f.ldy % kProdRows == 0, TTB_ERR_CAPABILITY, "TSQR apply: tile rows not a multiple of 128");
-  pa.unit_rows = ProductUnit::smem(f.ldy, b, k) <= 200 * 1024 ? f.ldy : kProdRows;
+  TTB_CHECK(f.ldy % kYUnit == 0, TTB_ERR_CAPABILITY, "TSQR apply: tile rows not a multiple of 128");
+  pa.unit_rows = kYUnit;
   const size_t psmem = ProductUnit::smem(pa.unit_rows, b, k);
   ProfScope ps("apply_product", ctx.stream);
   const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);

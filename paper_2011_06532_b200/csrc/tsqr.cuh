@@ -571,6 +571,37 @@ __device__ void store_Y(const double (&A)[C::RPL][C::CPL], int b, bool head, dou
   }
 }
 
+// Leaf Householder vectors in global memory, unit-major: a tile of MC rows is
+// MC / kYUnit units of kYUnit rows, each unit column-major with the padded
+// leading dimension kYLd, so one unit is ONE contiguous block (a single bulk
+// copy for the apply product) whose shared-memory image has conflict-free
+// MMA fragment loads (kYLd = 4 mod 16).
+constexpr int kYUnit = 128;
+constexpr int kYLd = kYUnit + 4;
+__host__ __device__ __forceinline__ int64_t y_tile_stride(int mc, int b) { return (int64_t)(mc / kYUnit) * b * kYLd; }
+__host__ __device__ __forceinline__ int64_t y_index(int r, int k, int b) {
+  return ((int64_t)(r / kYUnit) * b + k) * kYLd + (r % kYUnit);
+}
+
+template <class C>
+__device__ void store_Y_units(const double (&A)[C::RPL][C::CPL], int b, bool head, double* Y) {
+  static_assert(C::MC % kYUnit == 0, "leaf tiles are whole units");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lc = lane / C::LR, lr = lane % C::LR;
+#pragma unroll
+  for (int t = 0; t < C::CPL; ++t) {
+    const int k = col_of<C>(t, warp, lc);
+    if (k >= b) continue;
+#pragma unroll
+    for (int s = 0; s < C::RPL; ++s) {
+      const int r = C::row(s, lr);
+      double v = A[s][t];
+      if (head) v = r < k ? 0.0 : (r == k ? 1.0 : v);
+      Y[y_index(r, k, b)] = v;
+    }
+  }
+}
+
 template <class C>
 __device__ void store_T(const TileSmem<C>& sm, int b, double* T) {
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {

@@ -62,6 +62,7 @@ def main():
         rows.append((f"cfg2 orthonormalize {direction}", ms, 2 * bx, None))
     del x, z
     torch.cuda.empty_cache()
+    T.empty_cache()
 
     def rounding(name, x, opts, out_ranks, reps=3):
         ms, out = timed(lambda: T.round_tt(x, opts), reps=reps)
@@ -77,6 +78,7 @@ def main():
         rounding(name, T.add(y, y), T.RoundingOptions(1e-10), rk)
         del y
     torch.cuda.empty_cache()
+    T.empty_cache()
 
     # cfg4: X = 1.0 Y + 0.5 Z - 0.25 Y, dims [2^24, 64^4, 2^20], 60 -> 40
     dims = (1 << 24, 64, 64, 64, 64, 1 << 20)
@@ -87,6 +89,7 @@ def main():
     rounding("cfg4 round", x, T.RoundingOptions(1e-8), (1,) + (40,) * 5 + (1,))
     del x
     torch.cuda.empty_cache()
+    T.empty_cache()
 
     # cfg5: X o W, d=12, n=50000, r=8 -> 64, round(max_rank=32, eps0=0)
     dims, r = (50_000,) * 12, (1,) + (8,) * 11 + (1,)
@@ -108,10 +111,12 @@ def main():
     rows.append(("cfg5 hadamard (kernel time)", tot / 3, core_bytes(dims, r) * 2 + core_bytes(dims, p.ranks), None))
     del x, w
     torch.cuda.empty_cache()
+    T.empty_cache()
     rounding("cfg5 round (cap 32)", p, T.RoundingOptions(0.0, "LRLI", max_rank=32), (1,) + (32,) * 11 + (1,))
 
     del p
     torch.cuda.empty_cache()
+    T.empty_cache()
 
     # §8(f) row 2: Kronecker-sum (Laplacian) apply, d=8, n=20000, r=8 -> 64,
     # then apply + round(1e-10) (the Krylov caller; exact ranks <= 2r = 16)
