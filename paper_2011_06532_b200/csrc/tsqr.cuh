@@ -57,10 +57,10 @@ struct TCfg {
 #define TTB_LEAF64 8, 2, 4, 16
 #endif
 #ifndef TTB_LEAF32
-#define TTB_LEAF32 8, 4, 1, 16
+#define TTB_LEAF32 8, 1, 4, 16
 #endif
 #ifndef TTB_LEAF16
-#define TTB_LEAF16 8, 2, 1, 16
+#define TTB_LEAF16 8, 1, 2, 32
 #endif
 #ifndef TTB_TREE64
 #define TTB_TREE64 8, 2, 4, 16
@@ -72,8 +72,8 @@ struct TCfg {
 #define TTB_TREE16 8, 2, 1, 32
 #endif
 using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 256 threads (4 columns each), 1 CTA / SM
-using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 128-row tiles
-using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 256-row tiles
+using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 512-row tiles, 32 lanes per column
+using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 1024-row tiles, 32 lanes per column
 using Tree64 = TCfg<TTB_TREE64>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
 using Tree32 = TCfg<TTB_TREE32>;   // 256 rows: fan-in 8 at b = 32
 using Tree16 = TCfg<TTB_TREE16>;   // 512 rows: fan-in 32 at b = 16
