@@ -330,6 +330,154 @@ __global__ void __launch_bounds__(NT, 1) gram2_kernel(Gram2Args a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rank-16 specialisation (every rank 16: the interior cores of BASELINE
+// cfg2) on the m16n8k8 fp64 MMA: a whole 16 x 16 Z^T and accumulator per
+// warp, W^T fragments held in registers for the whole launch, 8 MMAs and 12
+// shared loads per slice (the generic kernel issues 32 m8n8k4 and ~50
+// loads).  Z^T(b, c) = sum_a X(a, ii, b) W(c, a) as (M = b, N = c, K = a);
+// acc(d, b) += sum_c Y(c, ii, d) Z(c, ii, b) as (M = d, N = b, K = c) with
+// the contraction index permuted inside each 8-block (k = t <-> c = 2t,
+// k = t + 4 <-> c = 2t + 1) so the D fragments of Z^T are directly the B
+// fragments of the second product.  Slices stream through a 3-stage
+// bulk-copy pipeline (one copy per right index, 16-slice chunks).
+// ---------------------------------------------------------------------------
+#ifndef TTB_G16_NS
+#define TTB_G16_NS 16
+#endif
+#ifndef TTB_G16_STAGES
+#define TTB_G16_STAGES 3
+#endif
+#ifndef TTB_G16_NT
+#define TTB_G16_NT 512
+#endif
+constexpr int kG16NS = TTB_G16_NS;           // slices per chunk
+constexpr int kG16Stages = TTB_G16_STAGES;
+constexpr int kG16NT = TTB_G16_NT;           // warps take the chunk's slices round-robin
+constexpr int kG16Ldx = 16 * kG16NS + 4;     // 4 mod 16: conflict-free scalar A loads
+constexpr int kG16Ldy = 16 * kG16NS + 8;     // 8 mod 16: conflict-free 16-byte A loads
+constexpr int kG16Stage = 16 * kG16Ldx + 16 * kG16Ldy;
+
+__device__ __forceinline__ void dmma1688(double (&d)[4], double a0, double a1, double a2, double a3, double b0,
+                                         double b1) {
+  asm(  // not volatile: the compiler may interleave independent products
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+
+__global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restrict__ W, const double* __restrict__ X,
+                                                           const double* __restrict__ Y, int64_t I, int64_t per_cta,
+                                                           double* __restrict__ part) {
+  extern __shared__ __align__(128) double g16[];
+  constexpr int NW = kG16NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(g16);
+  double* St = g16 + 16;  // stages: X block (16 x kG16Ldx), then Y block (16 x kG16Ldy)
+  if (tid < kG16Stages) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g2_smem(&bar[tid])) : "memory");
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  // W^T B fragments: (k = a, n = c) -> W(c, a) = W[c + 16 a]
+  double wf[2][2][2];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      wf[ks][nt][0] = W[(8 * nt + g) + 16 * (8 * ks + t)];
+      wf[ks][nt][1] = W[(8 * nt + g) + 16 * (8 * ks + t + 4)];
+    }
+  const int64_t s_begin = (int64_t)blockIdx.x * per_cta;
+  const int64_t s_end = min64(I, s_begin + per_cta);
+  const int nch = s_end > s_begin ? (int)((s_end - s_begin + kG16NS - 1) / kG16NS) : 0;
+  __syncthreads();
+  auto issue = [&](int c, int st) {  // warp 0: one bulk copy per right index of X and of Y
+    if (warp != 0) return;
+    const int64_t i0 = s_begin + (int64_t)c * kG16NS;
+    const int nn = (int)min64(kG16NS, s_end - i0);
+    const unsigned bytes = (unsigned)(16 * nn * 8);
+    if (lane == 0) g2_expect(&bar[st], 32 * bytes);
+    __syncwarp();
+    double* xs = St + (int64_t)st * kG16Stage;
+    double* ys = xs + 16 * kG16Ldx;
+    if (lane < 16) g2_bulk(xs + (int64_t)lane * kG16Ldx, X + 16 * (i0 + I * lane), bytes, &bar[st]);
+    else g2_bulk(ys + (int64_t)(lane - 16) * kG16Ldy, Y + 16 * (i0 + I * (lane - 16)), bytes, &bar[st]);
+  };
+  for (int c = 0; c < kG16Stages && c < nch; ++c) issue(c, c);
+  double acc[2][2][4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int bt = 0; bt < 2; ++bt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][bt][q] = 0.0;
+  for (int c = 0, st = 0, ph = 0; c < nch; ++c) {
+    const int64_t i0 = s_begin + (int64_t)c * kG16NS;
+    const int nn = (int)min64(kG16NS, s_end - i0);
+    g2_wait(&bar[st], ph);
+    const double* xs = St + (int64_t)st * kG16Stage;
+    const double* ys = xs + 16 * kG16Ldx;
+    // slices in pairs: both Z^T first, then both accumulations (two
+    // accumulator sets: independent MMA chains the scheduler can overlap)
+    auto zt = [&](int ii, double (&z)[2][4]) {  // Z^T (16 x 16): M = b, N = c, K = a
+      const double* xp = xs + 16 * ii;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) z[nt][q] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int a = 8 * ks + t;
+        const double a0 = xp[(int64_t)g * kG16Ldx + a], a1 = xp[(int64_t)(g + 8) * kG16Ldx + a];
+        const double a2 = xp[(int64_t)g * kG16Ldx + a + 4], a3 = xp[(int64_t)(g + 8) * kG16Ldx + a + 4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma1688(z[nt], a0, a1, a2, a3, wf[ks][nt][0], wf[ks][nt][1]);
+      }
+    };
+    auto accum = [&](int ii, const double (&z)[2][4], double (&ac)[2][4]) {  // acc(d, b) += Y(c, d) Z(c, b)
+      const double* yp = ys + 16 * ii;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        const double2 y0 = *reinterpret_cast<const double2*>(yp + (int64_t)g * kG16Ldy + 8 * kc + 2 * t);
+        const double2 y1 = *reinterpret_cast<const double2*>(yp + (int64_t)(g + 8) * kG16Ldy + 8 * kc + 2 * t);
+        dmma1688(ac[0], y0.x, y1.x, y0.y, y1.y, z[kc][0], z[kc][1]);
+        dmma1688(ac[1], y0.x, y1.x, y0.y, y1.y, z[kc][2], z[kc][3]);
+      }
+    };
+    for (int ii = warp; ii < nn; ii += 2 * NW) {
+      double z0[2][4], z1[2][4];
+      const bool two = ii + NW < nn;
+      zt(ii, z0);
+      if (two) zt(ii + NW, z1);
+      accum(ii, z0, acc[0]);
+      if (two) accum(ii + NW, z1, acc[1]);
+    }
+    __syncthreads();  // stage st is free
+    if (c + kG16Stages < nch) {
+      if (warp == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(c + kG16Stages, st);
+    }
+    if (++st == kG16Stages) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+  // per-warp 16 x 16 partials, summed over warps in a fixed order
+  double* red = St;  // NW x 256
+#pragma unroll
+  for (int bt = 0; bt < 2; ++bt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = g + 8 * (q >> 1), b = 8 * bt + 2 * t + (q & 1);
+      red[warp * 256 + d + 16 * b] = acc[0][bt][q] + acc[1][bt][q];
+    }
+  __syncthreads();
+  for (int e = tid; e < 256; e += kG16NT) {
+    double sum = 0.0;
+    for (int w = 0; w < NW; ++w) sum += red[w * 256 + e];
+    part[(int64_t)blockIdx.x * 256 + e] = sum;
+  }
+}
+
 __global__ void gram_final_kernel(const double* __restrict__ part, int nparts, int cnt, double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += blockDim.x * gridDim.x) {
     double s = 0.0;
@@ -347,6 +495,27 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
     return;
   }
   const bool even = (ral % 2 == 0) && (rbl % 2 == 0) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
+  static const bool no16 = getenv("TTB_GRAM_NO16") != nullptr;
+  if (even && !no16 && ral == 16 && rar == 16 && rbl == 16 && rbr == 16 && getenv("TTB_GRAM_V1") == nullptr) {
+    const size_t smem = (16 + (size_t)kG16Stages * kG16Stage) * sizeof(double);
+    int grid = (int)std::min<int64_t>((int64_t)ctx.num_sms, (I + kG16NS - 1) / kG16NS);
+    int64_t per_cta = (I + grid - 1) / grid;
+    per_cta = (per_cta + kG16NS - 1) / kG16NS * kG16NS;
+    grid = (int)((I + per_cta - 1) / per_cta);
+    double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
+    static bool attr = false;
+    if (!attr) {
+      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    ProfScope ps("gram", ctx.stream);
+    gram16_kernel<<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, I, per_cta, part);
+    TTB_LAUNCHED();
+    gram_final_kernel<<<1, 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
+    TTB_LAUNCHED();
+    ctx.free(part);
+    return;
+  }
   if (even && getenv("TTB_GRAM_V1") == nullptr) {
     Gram2Args g;
     g.W = W;
