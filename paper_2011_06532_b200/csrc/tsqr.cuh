@@ -389,12 +389,16 @@ constexpr int kSlot = T < C::CPL ? T : C::CPL - 1;
 
 template <class C, bool HEAD>
 __device__ __forceinline__ void publish(double (&A)[C::RPL][C::CPL], int j, int gj, TileSmem<C>& sm) {
-  static_assert(C::CPL <= 4, "slot dispatch handles CPL <= 4");
+  static_assert(C::CPL <= 8, "slot dispatch handles CPL <= 8");
   switch (C::owner_slot(j)) {
     case 0: publish_slot<C, HEAD, 0>(A, j, gj, sm); break;
     case 1: publish_slot<C, HEAD, kSlot<C, 1>>(A, j, gj, sm); break;
     case 2: publish_slot<C, HEAD, kSlot<C, 2>>(A, j, gj, sm); break;
-    default: publish_slot<C, HEAD, kSlot<C, 3>>(A, j, gj, sm); break;
+    case 3: publish_slot<C, HEAD, kSlot<C, 3>>(A, j, gj, sm); break;
+    case 4: publish_slot<C, HEAD, kSlot<C, 4>>(A, j, gj, sm); break;
+    case 5: publish_slot<C, HEAD, kSlot<C, 5>>(A, j, gj, sm); break;
+    case 6: publish_slot<C, HEAD, kSlot<C, 6>>(A, j, gj, sm); break;
+    default: publish_slot<C, HEAD, kSlot<C, 7>>(A, j, gj, sm); break;
   }
 }
 
@@ -518,7 +522,11 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
         case 0: TTB_UPD(0); break;
         case 1: TTB_UPD(T1); break;
         case 2: TTB_UPD((kSlot<C, 2>)); break;
-        default: TTB_UPD((kSlot<C, 3>)); break;
+        case 3: TTB_UPD((kSlot<C, 3>)); break;
+        case 4: TTB_UPD((kSlot<C, 4>)); break;
+        case 5: TTB_UPD((kSlot<C, 5>)); break;
+        case 6: TTB_UPD((kSlot<C, 6>)); break;
+        default: TTB_UPD((kSlot<C, 7>)); break;
       }
       publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
@@ -530,6 +538,10 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
     if (CPL > 1 && tn != 1) TTB_UPD(T1);
     if (CPL > 2 && tn != 2) TTB_UPD((kSlot<C, 2>));
     if (CPL > 3 && tn != 3) TTB_UPD((kSlot<C, 3>));
+    if (CPL > 4 && tn != 4) TTB_UPD((kSlot<C, 4>));
+    if (CPL > 5 && tn != 5) TTB_UPD((kSlot<C, 5>));
+    if (CPL > 6 && tn != 6) TTB_UPD((kSlot<C, 6>));
+    if (CPL > 7 && tn != 7) TTB_UPD((kSlot<C, 7>));
 #endif
 #undef TTB_UPD
 #pragma unroll
