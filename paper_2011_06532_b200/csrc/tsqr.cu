@@ -510,6 +510,7 @@ struct ProductArgs {
   LeafPlan plan;
   int ldy;
   int unit_rows;
+  int stages;
   const double* Y;
   const double* u;
   const double* z0;
@@ -523,12 +524,12 @@ struct ProductArgs {
 // (a unit = 128 rows of one tile) with a two-stage bulk-copy pipeline: unit
 // i+1's rows of Y_t and its u_t stream into shared memory while unit i is
 // multiplied.
-constexpr int kProdStages = 2;
+constexpr int kProdMaxStages = 8;  // stage count: as many units as fit ~200 KB (>= 2)
 
 struct ProductUnit {
   int rows;  // rows per work unit (kYUnit)
   __host__ __device__ static size_t smem(int ur, int b, int k) {
-    return 128 + (size_t)kProdStages * ((size_t)(ur + 4) * b + (size_t)b * ldpad(k)) * sizeof(double);
+    return ((size_t)(ur + 4) * b + (size_t)b * ldpad(k)) * sizeof(double);  // one stage
   }
 };
 
@@ -560,10 +561,12 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
   double* Ysb = reinterpret_cast<double*>(smem_raw + 128);
   const int64_t ystage = (int64_t)lys * b, ustage = (int64_t)b * ldu;
-  double* Usb = Ysb + kProdStages * ystage;
+  const int S = a.stages;
+  double* Usb = Ysb + S * ystage;
+  int64_t* rowoff = reinterpret_cast<int64_t*>(Usb + S * ustage);  // kYUnit entries
   const unsigned ubytes = (unsigned)(ustage * 8);
   if (threadIdx.x == 0) {
-    for (int s2 = 0; s2 < kProdStages; ++s2) mbar_init(&bar[s2], 1);
+    for (int s2 = 0; s2 < S; ++s2) mbar_init(&bar[s2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -582,13 +585,14 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
     }
   };
   int64_t unit = blockIdx.x;
-  if (unit < nunits) issue(unit, 0);
+  for (int s2 = 0; s2 < S - 1; ++s2)  // S - 1 units in flight ahead of the one being multiplied
+    if (unit + (int64_t)s2 * gridDim.x < nunits) issue(unit + (int64_t)s2 * gridDim.x, s2);
   for (int it = 0; unit < nunits; ++it, unit += gridDim.x) {
-    const int st = it & 1;
-    const int64_t nxt = unit + gridDim.x;
-    if (nxt < nunits) {  // stage st^1 was released by the barrier that ended the previous unit
+    const int st = it % S;
+    const int64_t nxt = unit + (int64_t)(S - 1) * gridDim.x;
+    if (nxt < nunits) {  // its stage was released by the barrier that ended the previous unit
       if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(nxt, st ^ 1);
+      issue(nxt, (it + S - 1) % S);
     }
     const int64_t tile = unit / halves;
     const int r0 = (int)(unit - tile * halves) * UR;
@@ -603,17 +607,28 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
     const double* z0 = a.z0 + (int64_t)g * b * k;
     const double* Ys = Ysb + st * ystage;
     const double* Us = Usb + st * ustage;
-    mbar_wait(&bar[st], (it >> 1) & 1);
-    if (rows > 0)
+    // output address of unit row m: rowoff[m] + n * cstride (one division per
+    // row here instead of one per element in the epilogue)
+    const int64_t cstride = a.out.trans ? 1 : a.out.rl * a.out.I;
+    for (int m = threadIdx.x; m < rows; m += kProdNT) {
+      int si, w;
+      tile_row(a.out.trans, r0 + m, nsl, rs, si, w);
+      rowoff[m] = a.out.addr(w, ia + si, 0);
+    }
+    mbar_wait(&bar[st], (it / S) & 1);
+    __syncthreads();
+    if (rows > 0) {
+      double* ob = a.out.base;
+      // Y rows beyond `rows` are exact zeros (zero-padded leaf tiles), so only
+      // the reflector index needs a bound
       cta_dmma(
-          rows, k, b, NW, [&](int m, int l) { return (m < rows && l < b) ? Ys[m + lys * l] : 0.0; },
+          rows, k, b, NW, [&](int m, int l) { return l < b ? Ys[m + lys * l] : 0.0; },
           [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
           [&](int m, int n, double v) {
             const double base = (head && m < b) ? z0[m + b * n] : 0.0;
-            int si, w;
-            tile_row(a.out.trans, r0 + m, nsl, rs, si, w);
-            a.out.base[a.out.addr(w, ia + si, n)] = base - v;
+            ob[rowoff[m] + cstride * n] = base - v;
           });
+    }
     __syncthreads();
   }
 }
@@ -886,7 +901,9 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.out = out;
   TTB_CHECK(f.ldy % kYUnit == 0, TTB_ERR_CAPABILITY, "TSQR apply: tile rows not a multiple of 128");
   pa.unit_rows = kYUnit;
-  const size_t psmem = ProductUnit::smem(pa.unit_rows, b, k);
+  const size_t pstage = ProductUnit::smem(pa.unit_rows, b, k);
+  pa.stages = (int)std::max<size_t>(2, std::min<size_t>(kProdMaxStages, (200 * 1024) / pstage));
+  const size_t psmem = 128 + (size_t)pa.stages * pstage + kYUnit * sizeof(int64_t);
   ProfScope ps("apply_product", ctx.stream);
   const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);
   const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunits, ctx.num_sms));
