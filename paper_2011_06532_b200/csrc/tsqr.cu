@@ -135,12 +135,12 @@ extern "C" int ttb_dbg_tclk(unsigned long long* out) {
 #endif
 
 // Column-loop hooks of a tree node.
-//  inputs: complete (level 0: loaded whole at the start) or streamed: warp
-//    0 polls the children's progress counters one step ahead (the acquire
-//    load is issued at the start of a step and tested at its end) and, when
-//    a chunk of rows is final in every child, lane c bulk-copies child c's
-//    rows into the shared staging area (one mbarrier per chunk); the other
-//    warps wait on that barrier only when they reach the chunk.
+//  inputs: complete (level 0: loaded whole at the start) or streamed: a
+//    data-mover warp (its own warpgroup, registers handed to the compute
+//    warps with setmaxnreg) polls the children's progress counters and, as
+//    soon as a chunk of rows is final in every child, lane c bulk-copies
+//    child c's rows into the shared staging area (one mbarrier per chunk);
+//    the compute warps wait on that barrier only when they reach the chunk.
 //  outputs: after step j every warp writes row j of R (its columns) into
 //    the node's row-major stream and, per finished chunk, bumps the node's
 //    progress counter.
@@ -154,8 +154,6 @@ struct TreeHooks {
   double* stage;            // shared: MC x ldr
   unsigned long long* sbar; // shared: one per chunk
   int c0, cnt, b, ldr, nchunks;
-  int next;                 // warp 0: next chunk to issue
-  unsigned pv;              // warp 0: pending progress value
 
   __device__ __forceinline__ unsigned need(int ci) const { return (unsigned)C::NW * (unsigned)(ci + 1); }
   __device__ __forceinline__ void issue(int ci) {
@@ -168,23 +166,20 @@ struct TreeHooks {
     for (int c = lane; c < cnt; c += 32)
       bulk_g2s(stage + ((int64_t)c * b + j0) * ldr, Rrow_in + ((int64_t)(c0 + c) * b + j0) * ldr, bytes, &sbar[ci]);
   }
-  // warp 0, blocking: issue every chunk that is already final (start-up)
-  __device__ __forceinline__ void poll_blocking(int upto) {
+  // the data-mover warp (C::XW) issues every chunk as soon as it is final
+  // in every child; the compute warps never poll or fence for inputs
+  __device__ __forceinline__ void mover() {
+    if (!prog_in) return;
     const int lane = threadIdx.x & 31;
-    while (next < nchunks && next <= upto) {
+    for (int ci = 0; ci < nchunks; ++ci) {
       for (int c = lane; c < cnt; c += 32)
-        while (ld_acquire(prog_in + c) < need(next)) {
+        while (ld_acquire(prog_in + c) < need(ci)) {
         }
       __syncwarp();
-      issue(next++);
+      issue(ci);
     }
   }
-  __device__ __forceinline__ void pre(int) {
-    if (!prog_in || (threadIdx.x >> 5) != 0 || next >= nchunks) return;
-    const int lane = threadIdx.x & 31;
-    pv = 0xffffffffu;
-    for (int c = lane; c < cnt; c += 32) pv = min(pv, ld_relaxed(prog_in + c));
-  }
+  __device__ __forceinline__ void pre(int) {}
   template <class T>
   __device__ __forceinline__ void feed(T& A, int j0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -204,7 +199,6 @@ struct TreeHooks {
       return;
     }
     const int ci = j0 / kTreeChunk;
-    if (warp == 0) poll_blocking(ci);  // never blocks in steady state
     mbar_wait(&sbar[ci], 0);
     const int j1 = min(j0 + kTreeChunk, b);
 #pragma unroll
@@ -225,13 +219,6 @@ struct TreeHooks {
 #ifdef TTB_TCLK2
     if (lane == 0 && warp == 0) TTB_TSTAMP(j);
 #endif
-    if (prog_in && warp == 0 && next < nchunks) {  // test the poll issued in pre()
-      const bool ok = __all_sync(0xffffffffu, pv >= need(next));
-      if (ok) {
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-        issue(next++);
-      }
-    }
     if (!prog_out) return;
     const int lc = lane / C::LR, lr = lane % C::LR;
     const int sj = 2 * (j / (2 * C::LR)) + (j & 1), lrj = (j % (2 * C::LR)) / 2;
@@ -259,7 +246,7 @@ struct TreeHooks {
 };
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, 1) tsqr_tree_kernel(TreePlan tp) {
+__global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
   unsigned long long* sbar = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(TileSmem<C>) + 127) & ~size_t(127)));
@@ -298,13 +285,21 @@ __global__ void __launch_bounds__(C::NT, 1) tsqr_tree_kernel(TreePlan tp) {
   h.b = b;
   h.ldr = tp.ldr;
   h.nchunks = nchunks;
-  h.next = 0;
-  h.pv = 0;
+  // warp specialisation: the extra warpgroup moves the children's rows (one
+  // warp of it is enough) and hands its registers to the compute warps, which
+  // hold the 256 x 64 register tile
+  static_assert(C::XW == 4 && C::NW % 4 == 0, "whole warpgroups");
+  if (threadIdx.x >= C::NT) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (threadIdx.x < C::NT + 32) h.mover();
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   tile_qr_t<C, true>(A, b, sm, 0, h);
   store_Y<C>(A, b, true, tp.Y[L] + (int64_t)q * C::MC * b, C::MC);
   store_T<C>(sm, b, tp.T[L] + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
   extract_R<C>(A, b, sm);
-  __syncthreads();
+  C::sync();
   double* Rout = tp.R[L] + (int64_t)q * b * b;
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
     const int r = idx % b, k = idx / b;
@@ -701,7 +696,7 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     TTB_CHECK((f.b + kTreeChunk - 1) / kTreeChunk <= kMaxChunks, TTB_ERR_CAPABILITY, "TSQR tree: too many chunks");
     TTB_CUDA(cudaMemsetAsync(f.prog, 0, sizeof(unsigned) * total, st));
     ProfScope ps("tsqr_tree", st);
-    tree<<<total, TC_::NT, tree_smem<TC_>(), st>>>(tp);
+    tree<<<total, TC_::NTT, tree_smem<TC_>(), st>>>(tp);
     TTB_LAUNCHED();
     return rin;
   };

@@ -29,10 +29,20 @@
 
 namespace ttb {
 
-template <int NW_, int LC_, int CPL_, int RPL_>
+// XW_: extra warps of the CTA beyond the NW compute warps (the tree's data
+// mover); the tile routines then synchronise the compute warps only.
+template <int NW_, int LC_, int CPL_, int RPL_, int XW_ = 0>
 struct TCfg {
-  static constexpr int NW = NW_, LC = LC_, LR = 32 / LC_, CPL = CPL_, RPL = RPL_;
-  static constexpr int NT = NW * 32;
+  static constexpr int NW = NW_, LC = LC_, LR = 32 / LC_, CPL = CPL_, RPL = RPL_, XW = XW_;
+  static constexpr int NT = NW * 32;        // compute threads (the first NT of the CTA)
+  static constexpr int NTT = NT + 32 * XW;  // all threads of the CTA
+  __device__ __forceinline__ static void sync() {
+    if (XW == 0) {
+      __syncthreads();
+    } else {
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+    }
+  }
   static constexpr int BMAX = NW * LC * CPL;
   static constexpr int MC = LR * RPL;
   // resident CTAs per SM: two only when the register tile leaves room
@@ -74,9 +84,9 @@ struct TCfg {
 using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 256 threads (4 columns each), 1 CTA / SM
 using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 512-row tiles, 32 lanes per column
 using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 1024-row tiles, 32 lanes per column
-using Tree64 = TCfg<TTB_TREE64>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
-using Tree32 = TCfg<TTB_TREE32>;   // 256 rows: fan-in 8 at b = 32
-using Tree16 = TCfg<TTB_TREE16>;   // 512 rows: fan-in 32 at b = 16
+using Tree64 = TCfg<TTB_TREE64, 4>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
+using Tree32 = TCfg<TTB_TREE32, 4>;   // 256 rows: fan-in 8 at b = 32
+using Tree16 = TCfg<TTB_TREE16, 4>;   // 512 rows: fan-in 32 at b = 16
 
 // A row-sliced view of an F-order slab (rl, I, rr):
 //   trans == 0: V(X)    rows per slice rs = rl, columns = rr
@@ -243,7 +253,7 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
   int BP = 1;
   while (BP < b) BP <<= 1;
   for (int k = tid; k < BP; k += C::NT) sm.Gs[k + BM * k] = (k < b) ? sm.taus[k] : 1.0;
-  __syncthreads();
+  C::sync();
   for (int s = 1; s < BP; s <<= 1) {
     const int nblk = BP / (2 * s);
     const int items = nblk * s * s;
@@ -256,7 +266,7 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
       for (int l = 0; l <= c; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (c0 + l)], sm.Gs[(c0 + l) + BM * (c0 + c)], acc);
       sm.Xs[idx] = acc;
     }
-    __syncthreads();
+    C::sync();
     // T[A,C] = -T[A,A] * X
     for (int idx = tid; idx < items; idx += C::NT) {
       int q = idx / (s * s), rem = idx - q * s * s;
@@ -266,7 +276,7 @@ __device__ void build_T(TileSmem<C>& sm, int b) {
       for (int l = r; l < s; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (a0 + l)], sm.Xs[q * s * s + l + s * c], acc);
       sm.Gs[(a0 + r) + BM * (c0 + c)] = -acc;
     }
-    __syncthreads();
+    C::sync();
   }
 }
 
@@ -549,7 +559,7 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       if (kk[t] < j && lr == 0) sm.Gs[kk[t] + BM * j] = d[t];
     h.post(A, j);
   }
-  __syncthreads();
+  C::sync();
   build_T<C>(sm, b);
 }
 
