@@ -85,6 +85,38 @@ def _worker(rank, world, port, q):
         res["inner"] = float(w[0, 0])
         res["inner_ref"] = O.inner(x, y)
         res["bytes"] = rounding_bytes((4, 4), (1, 2, 1), (1, 1, 1))
+        # 5. Kronecker-operator halo exchange (ops.py:270-311): the package's
+        #    transfer plan, payloads swapped point to point over the group
+        #    (the device path packs with ttb_gather_slices and swaps them with
+        #    one grouped NCCL send/recv), renumbered CSR rows applied locally
+        import scipy.sparse as sp
+        import torch
+        from paper_2011_06532_b200.operator import exchange_plan
+        core = O.random_cores((13,), (1, 1), 5)[0]
+        core = np.asfortranarray(np.repeat(core, 6, axis=0).reshape(2, 13, 3, order="F") * 1.5)
+        ok = True
+        for a in (sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(13, 13), format="csr"),
+                  sp.csr_matrix((np.ones(13), (np.arange(13), (np.arange(13) + 5) % 13)), shape=(13, 13)),
+                  sp.random(13, 13, density=0.3, random_state=9, format="csr")):
+            pl = exchange_plan(a, world, rank)
+            mine = core[:, pl.lo:pl.hi, :]
+            reqs, bufs = [], []
+            for qq, idx in sorted(pl.send.items()):
+                payload = np.concatenate([mine[:, int(i), :].ravel(order="F") for i in idx])
+                reqs.append(dist.isend(torch.from_numpy(payload), dst=qq))
+            for qq, idx in sorted(pl.recv.items()):
+                buf = torch.empty(idx.size * 6, dtype=torch.float64)
+                reqs.append(dist.irecv(buf, src=qq))
+                bufs.append(buf)
+            for r_ in reqs:
+                r_.wait()
+            halo = [b.numpy().reshape(-1, 6) for b in bufs]
+            src = np.concatenate([np.stack([mine[:, i, :].ravel(order="F") for i in range(pl.nloc)])] + halo)
+            m = sp.csr_matrix((pl.vals, pl.cols, pl.indptr), shape=(pl.nloc, src.shape[0]))
+            rows = np.asarray(m @ src).reshape(pl.nloc, 3, 2).transpose(2, 0, 1)
+            got = np.concatenate(g.allgather_object(np.asfortranarray(rows)), axis=1)
+            ok = ok and np.array_equal(got, O.mode2_multiply(core, a))
+        res["operator_exchange"] = ok
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -110,6 +142,7 @@ def test_two_rank_host_logic():
         assert res["tsqr_err"] < 1e-12
         assert res["apply_err"] < 1e-12
         assert res["inner"] == pytest.approx(res["inner_ref"], rel=1e-12)
+        assert res["operator_exchange"]
     # the redundant results are identical on every rank
     assert out[0]["inner"] == out[1]["inner"]
     assert out[0]["tsqr_err"] == out[1]["tsqr_err"]
