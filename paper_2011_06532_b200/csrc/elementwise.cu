@@ -114,11 +114,14 @@ void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, 
 // Z(a*rbl + c, i, b*rbr + d) = X(a, i, b) * Y(c, i, d)
 __global__ void __launch_bounds__(kEwNT)
 hadamard_kernel(const double* __restrict__ x, int64_t ral, int64_t rar, const double* __restrict__ y, int64_t rbl,
-                int64_t rbr, int64_t I, int ni, double* __restrict__ out) {
-  const int64_t col = blockIdx.y;
+                int64_t rbr, int64_t I, int ni, int col_fast, double* __restrict__ out) {
+  // col_fast: the output column is blockIdx.x, so the CTAs of all columns of
+  // a slice run are dispatched together and re-read its input slices from L2
+  const int64_t col = col_fast ? blockIdx.x : blockIdx.y;
+  const int64_t run = col_fast ? blockIdx.y : blockIdx.x;
   const int64_t bx = col / rbr, dy = col - bx * rbr;
   const int64_t RL = ral * rbl;
-  const int64_t i0 = (int64_t)blockIdx.x * ni;
+  const int64_t i0 = run * ni;
   const int64_t nn = min64(ni, I - i0);
   double* o = out + RL * (i0 + I * col);
   const double* xs = x + ral * (i0 + I * bx);
@@ -138,9 +141,11 @@ void hadamard_core(Ctx& ctx, const double* x, int64_t ral, int64_t rar, const do
   if (I == 0) return;
   TTB_CHECK(RR <= 65535 && RL <= (1 << 24), TTB_ERR_CAPABILITY, "hadamard: output rank too large");
   int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
-  dim3 grid((unsigned)((I + ni - 1) / ni), (unsigned)RR);
+  const int64_t runs = (I + ni - 1) / ni;
+  const bool col_fast = runs <= 65535;
+  dim3 grid = col_fast ? dim3((unsigned)RR, (unsigned)runs) : dim3((unsigned)runs, (unsigned)RR);
   ProfScope ps("hadamard", ctx.stream);
-  hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, out);
+  hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, col_fast ? 1 : 0, out);
   TTB_LAUNCHED();
 }
 
