@@ -176,6 +176,16 @@ int ttb_mode2_spmm(ttb_ctx* ctx, int64_t rl, int64_t rr, int64_t nrows, const in
                    const int64_t* cols, const double* vals, int64_t nloc, const double* local,
                    const double* halo, double* out, int64_t out_rl, int64_t out_d, int64_t a0,
                    int64_t c0);
+/* A whole core of the summed operator (the TT sum of apply_operator's
+ * terms, ops.py:330-333) in one pass, every output cell written once:
+ * mode 0 interior core (nterms rl, nrows, nterms rr) block diagonal, term t
+ * in block (t, t); mode 1 first core (1, nrows, nterms rr), blocks side by
+ * side; mode 2 last core (nterms rl, nrows, 1), stacked.  Term t uses the
+ * CSR arrays indptr[t] / cols[t] / vals[t] and the halo buffer halo[t]
+ * (device pointers, as ttb_mode2_spmm); nterms <= 16. */
+int ttb_mode2_spmm_sum(ttb_ctx* ctx, int nterms, int mode, int64_t rl, int64_t rr, int64_t nrows,
+                       const int64_t* const* indptr, const int64_t* const* cols, const double* const* vals,
+                       int64_t nloc, const double* local, const double* const* halo, double* out);
 /* out (slice-major, n slices of rl x rr F-order) = slab(:, idx[k], :) for
  * the F-order slab (rl, I, rr); idx is a DEVICE int64 array.  Packs the
  * payload of the operator exchange (ops.py:284-287). */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "ttb_truncated_svd": (C.c_int, [_P, _I64, _I64, _P, C.c_double, _I64, _P, _P, _P, _PI64, _PD,
                                     C.POINTER(C.c_int)]),
     "ttb_mode2_spmm": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _I64, _I64]),
+    "ttb_mode2_spmm_sum": (C.c_int, [_P, C.c_int, C.c_int, _I64, _I64, _I64, _PP, _PP, _PP, _I64, _P, _PP, _P]),
     "ttb_gather_slices": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "ttb_exchange": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _PP, _PI64, _PP, _PI64]),
     "ttb_read_slabs": (C.c_int, [_P, C.c_char_p, _I64, C.c_int, _PI64, _PI64, _PI64, _PI64, _PP]),

@@ -59,6 +59,67 @@ mode2_spmm_kernel(int64_t rl, int64_t rr, int64_t nrows, const int64_t* __restri
   }
 }
 
+// One pass over a whole summed operator core: every output cell is written
+// once -- term t's product in its diagonal block, exact zeros elsewhere --
+// so the block-diagonal TT sum of the terms costs no separate zero fill.
+// mode 0: interior core (T rl, I, T rr), block diagonal; mode 1: first core
+// (1, I, T rr), blocks side by side; mode 2: last core (T rl, I, 1), stacked.
+constexpr int kSpMaxTerms = 16;
+struct SpmmTerms {
+  int nterms;
+  const int64_t* indptr[kSpMaxTerms];
+  const int64_t* cols[kSpMaxTerms];
+  const double* vals[kSpMaxTerms];
+  const double* halo[kSpMaxTerms];
+};
+
+__global__ void __launch_bounds__(kSpNT)
+mode2_spmm_sum_kernel(SpmmTerms st, int mode, int64_t rl, int64_t rr, int64_t nrows, int64_t nloc,
+                      const double* __restrict__ local, double* __restrict__ out, int64_t ORL, int ni) {
+  const int64_t C = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * ni;
+  const int nn = (int)min64(ni, nrows - i0);
+  const int tC = mode == 2 ? -1 : (int)(C / rr);
+  const int64_t c = mode == 2 ? 0 : C - (int64_t)tC * rr;
+  double* o = out + ORL * (i0 + nrows * C);
+  const int64_t hstride = rl * rr;
+  auto cell = [&](int A, int ii) {
+    int t;
+    int64_t a;
+    if (mode == 1) {
+      t = tC;
+      a = A;
+    } else {
+      t = (int)(A / rl);
+      a = A - (int64_t)t * rl;
+    }
+    double acc = 0.0;
+    if (mode == 2 || t == tC) {
+      const int64_t* ip = st.indptr[t] + i0;
+      const int64_t* cl = st.cols[t];
+      const double* vl = st.vals[t];
+      const double* loc = local + rl * nloc * c;
+      const double* hal = st.halo[t] + rl * c;
+      const int64_t beg = ip[ii], end = ip[ii + 1];
+      for (int64_t jj = beg; jj < end; ++jj) {
+        const int64_t j = cl[jj];
+        const double x = j < nloc ? loc[a + rl * j] : hal[a + hstride * (j - nloc)];
+        acc = __dadd_rn(acc, __dmul_rn(vl[jj], x));
+      }
+    }
+    o[A + ORL * ii] = acc;
+  };
+  if (ORL <= kSpNT) {
+    const int per = kSpNT / (int)ORL;
+    const int A = threadIdx.x % (int)ORL, g = threadIdx.x / (int)ORL;
+    if (g < per)
+      for (int ii = g; ii < nn; ii += per) cell(A, ii);
+  } else {
+    for (int ii = 0; ii < nn; ++ii)
+      for (int A = threadIdx.x; A < ORL; A += kSpNT) cell(A, ii);
+  }
+}
+
 __global__ void gather_slices_kernel(int64_t rl, int64_t I, int64_t rr, const double* __restrict__ slab, int64_t n,
                                      const int64_t* __restrict__ idx, double* __restrict__ out) {
   const int64_t per = rl * rr;
@@ -93,6 +154,38 @@ int ttb_mode2_spmm(ttb_ctx* ctx, int64_t rl, int64_t rr, int64_t nrows, const in
   ProfScope ps("mode2_spmm", c.stream);
   mode2_spmm_kernel<<<grid, kSpNT, 0, c.stream>>>(rl, rr, nrows, indptr, cols, vals, nloc, local, halo, out, out_rl,
                                                   out_d, a0, c0, ni);
+  TTB_LAUNCHED();
+  TTB_TRY_END
+}
+
+int ttb_mode2_spmm_sum(ttb_ctx* ctx, int nterms, int mode, int64_t rl, int64_t rr, int64_t nrows,
+                       const int64_t* const* indptr, const int64_t* const* cols, const double* const* vals,
+                       int64_t nloc, const double* local, const double* const* halo, double* out) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(ctx, TTB_ERR_CONTRACT, "null context");
+  TTB_CHECK(nterms >= 1 && nterms <= kSpMaxTerms, TTB_ERR_CAPABILITY, "mode2_spmm_sum: 1..16 terms");
+  TTB_CHECK(mode >= 0 && mode <= 2, TTB_ERR_CONTRACT, "mode2_spmm_sum: bad mode");
+  TTB_CHECK(rl >= 1 && rr >= 1 && nrows >= 0 && nloc >= 0, TTB_ERR_SHAPE, "mode2_spmm_sum: bad slab shape");
+  TTB_CHECK(mode != 1 || rl == 1, TTB_ERR_SHAPE, "mode2_spmm_sum: first core needs r_left 1");
+  TTB_CHECK(mode != 2 || rr == 1, TTB_ERR_SHAPE, "mode2_spmm_sum: last core needs r_right 1");
+  if (nrows == 0) return TTB_OK;
+  SpmmTerms st;
+  st.nterms = nterms;
+  for (int t = 0; t < nterms; ++t) {
+    st.indptr[t] = indptr[t];
+    st.cols[t] = cols[t];
+    st.vals[t] = vals[t];
+    st.halo[t] = halo[t];
+  }
+  const int64_t ORL = mode == 1 ? 1 : (int64_t)nterms * rl;
+  const int64_t ORR = mode == 2 ? 1 : (int64_t)nterms * rr;
+  TTB_CHECK(ORR <= 65535, TTB_ERR_CAPABILITY, "mode2_spmm_sum: output right rank above 65535");
+  Ctx& c = ctx->c;
+  int ni = (int)max64(1, kSpElems / ORL);
+  if (ni > nrows) ni = (int)nrows;
+  dim3 grid(ceil_div(nrows, ni), (unsigned)ORR);
+  ProfScope ps("mode2_spmm", c.stream);
+  mode2_spmm_sum_kernel<<<grid, kSpNT, 0, c.stream>>>(st, mode, rl, rr, nrows, nloc, local, out, ORL, ni);
   TTB_LAUNCHED();
   TTB_TRY_END
 }

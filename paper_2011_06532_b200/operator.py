@@ -197,9 +197,9 @@ def _spmm(comm, slab, t_op, plan_dev, out, a0, c0):
 
 def _apply_terms(op, dt: DistTTTensor) -> DistTTTensor:
     """sum_t (term t applied to dt), assembled block-diagonally in one pass
-    per core (equal to add(add(p0, p1), ...) of the reference, ops.py:330-333)."""
-    import torch
-
+    per core (equal to add(add(p0, p1), ...) of the reference, ops.py:330-333):
+    ttb_mode2_spmm_sum writes every output cell once, the products of term t
+    in its diagonal block and exact zeros elsewhere."""
     comm = dt.comm
     N, T = dt.ndim, len(op.terms)
     if N == 1 and T > 1:
@@ -207,19 +207,21 @@ def _apply_terms(op, dt: DistTTTensor) -> DistTTTensor:
 
         return add_n([_apply_terms(KroneckerOperator(op.dims, [f]), dt) for f in op.terms])
     ranks = (1,) + tuple(T * r for r in dt.ranks[1:-1]) + (1,)
+    lib = _lib.load()
     outs = []
     for n, slab in enumerate(dt.local):
         rl, dloc, rr = slab.shape
-        shape = (ranks[n], dloc, ranks[n + 1])
-        if 0 < n < N - 1 and T > 1:
-            o = torch.zeros(shape[0] * shape[1] * shape[2], dtype=torch.float64, device=comm.device)
-            o = o.as_strided(shape, (1, shape[0], shape[0] * shape[1]))
-        else:
-            o = f_empty(*shape, comm.device)
-        for t in range(T):
-            a0 = 0 if n == 0 else t * rl
-            c0 = 0 if n == N - 1 else t * rr
-            _spmm(comm, slab, op.terms[t][n], _dev_plan(op, t, n, comm), o, a0, c0)
+        o = f_empty(ranks[n], dloc, ranks[n + 1], comm.device)
+        plans = [_dev_plan(op, t, n, comm) for t in range(T)]
+        halos = [_halo(comm, slab, pd[0], pd[4]) for pd in plans]  # exchanges (P > 1), in term order
+        mode = 1 if n == 0 and N > 1 else (2 if n == N - 1 and N > 1 else 0)
+        if N == 1:
+            mode = 0  # single term on a single core: rl = rr = 1
+        _lib.check(lib.ttb_mode2_spmm_sum(
+            comm.ctx(), T, mode, rl, rr, dloc,
+            _lib.ptr_array([pd[1].data_ptr() for pd in plans]), _lib.ptr_array([pd[2].data_ptr() for pd in plans]),
+            _lib.ptr_array([pd[3].data_ptr() for pd in plans]), dloc, C.c_void_p(slab.data_ptr()),
+            _lib.ptr_array([h.data_ptr() for h in halos]), C.c_void_p(o.data_ptr())))
         outs.append(o)
     return DistTTTensor(comm, dt.dims, ranks, outs)
 
