@@ -506,6 +506,7 @@ struct ProductArgs {
   int ldy;
   int unit_rows;
   int stages;
+  int upw;
   const double* Y;
   const double* u;
   const double* z0;
@@ -548,17 +549,19 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
   constexpr int NW = kProdNT / 32;
   const LeafPlan& pl = a.plan;
   const int b = pl.b, k = a.k, ldy = a.ldy, rs = pl.rs, ni = pl.ni;
-  const int UR = kYUnit;
+  const int upw = a.upw;     // Y units per work item (consecutive, contiguous in global)
+  const int UR = kYUnit * upw;
   const int lys = kYLd;
+  const int64_t ustride = (int64_t)b * kYLd;  // one unit of Y
   const int ldu = ldpad(k);
   const int halves = ldy / UR;
   const int64_t nunits = pl.total_tiles() * halves;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
   double* Ysb = reinterpret_cast<double*>(smem_raw + 128);
-  const int64_t ystage = (int64_t)lys * b, ustage = (int64_t)b * ldu;
+  const int64_t ystage = ustride * upw, ustage = (int64_t)b * ldu;
   const int S = a.stages;
   double* Usb = Ysb + S * ystage;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(Usb + S * ustage);  // kYUnit entries
+  int64_t* rowoff = reinterpret_cast<int64_t*>(Usb + S * ustage);  // UR entries
   const unsigned ubytes = (unsigned)(ustage * 8);
   if (threadIdx.x == 0) {
     for (int s2 = 0; s2 < S; ++s2) mbar_init(&bar[s2], 1);
@@ -617,7 +620,7 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
       // Y rows beyond `rows` are exact zeros (zero-padded leaf tiles), so only
       // the reflector index needs a bound
       cta_dmma(
-          rows, k, b, NW, [&](int m, int l) { return l < b ? Ys[m + lys * l] : 0.0; },
+          rows, k, b, NW, [&](int m, int l) { return l < b ? Ys[(m >> 7) * ustride + (m & (kYUnit - 1)) + lys * l] : 0.0; },
           [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
           [&](int m, int n, double v) {
             const double base = (head && m < b) ? z0[m + b * n] : 0.0;
@@ -895,10 +898,14 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.k = k;
   pa.out = out;
   TTB_CHECK(f.ldy % kYUnit == 0, TTB_ERR_CAPABILITY, "TSQR apply: tile rows not a multiple of 128");
-  pa.unit_rows = kYUnit;
-  const size_t pstage = ProductUnit::smem(pa.unit_rows, b, k);
+  // small panels: several units per work item (more rows per CTA pass)
+  pa.upw = 1;
+  const size_t ubytes1 = (size_t)b * kYLd * sizeof(double);
+  while (pa.upw * 2 <= f.ldy / kYUnit && (size_t)(pa.upw * 2) * ubytes1 <= 72 * 1024) pa.upw *= 2;
+  pa.unit_rows = kYUnit * pa.upw;
+  const size_t pstage = (size_t)pa.upw * ubytes1 + (size_t)b * ldpad(k) * sizeof(double);
   pa.stages = (int)std::max<size_t>(2, std::min<size_t>(kProdMaxStages, (200 * 1024) / pstage));
-  const size_t psmem = 128 + (size_t)pa.stages * pstage + kYUnit * sizeof(int64_t);
+  const size_t psmem = 128 + (size_t)pa.stages * pstage + (size_t)pa.unit_rows * sizeof(int64_t);
   ProfScope ps("apply_product", ctx.stream);
   const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);
   const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunits, ctx.num_sms));
