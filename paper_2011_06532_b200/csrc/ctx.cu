@@ -192,6 +192,22 @@ void Ctx::read_small(const void* dev, size_t bytes, void* host) {
   memcpy(host, mapped_host, bytes);
 }
 
+int* Ctx::flag() {
+  if (!dflag) {
+    TTB_CUDA(cudaMalloc(&dflag, 256));
+    TTB_CUDA(cudaMemsetAsync(dflag, 0, 256, stream));
+  }
+  return dflag;
+}
+
+void Ctx::flag_reset() { TTB_CUDA(cudaMemsetAsync(flag(), 0, sizeof(int), stream)); }
+
+bool Ctx::flag_read() {
+  int h = 0;
+  read_small(flag(), sizeof(int), &h);
+  return h != 0;
+}
+
 cudaStream_t Ctx::copy_stream() {
   if (!copy) TTB_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
   return copy;
@@ -243,6 +259,7 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
     if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
     if (ctx->c.copy) cudaStreamDestroy(ctx->c.copy);
     if (ctx->c.mapped_host) cudaFreeHost(ctx->c.mapped_host);
+    if (ctx->c.dflag) cudaFree(ctx->c.dflag);
     delete ctx;
   }
   TTB_TRY_END

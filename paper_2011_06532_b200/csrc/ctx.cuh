@@ -34,6 +34,12 @@ struct Ctx {
   void* mapped_dev = nullptr;
   unsigned read_seq = 0;
   void read_small(const void* dev, size_t bytes, void* host);
+  // sticky device flag: set by kernels that meet non-finite data (TSQR R
+  // factors); reset / read once per API call
+  int* dflag = nullptr;
+  int* flag();
+  void flag_reset();
+  bool flag_read();
   void* alloc(size_t bytes);
   void free(void* p);
   // free memory last used on another stream: the block goes back to the

@@ -212,6 +212,7 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
     copy_d2d(ctx, out[0], in[0], ranks[0] * dims[0] * ranks[1]);
     return TTB_OK;
   }
+  ctx.flag_reset();
   if (direction == 0) {
     const double* work = in[0];
     for (int n = 0; n < N - 1; ++n) {
@@ -239,6 +240,7 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
       work = out[n - 1];
     }
   }
+  TTB_CHECK(!ctx.flag_read(), TTB_ERR_NUMERIC, "non-finite entries in the tensor (orthonormalization)");
   TTB_TRY_END
 }
 
@@ -595,7 +597,12 @@ int ttb_tsqr_factor(ttb_ctx* h, int64_t rl, int64_t I, int64_t rr, int trans, co
   TTB_CHECK(out, TTB_ERR_CONTRACT, "null factor handle");
   ttb_tsqr* f = new ttb_tsqr();
   try {
+    ctx.flag_reset();
     tsqr_factor(ctx, panel_of(slab, rl, I, rr, trans ? 1 : 0), f->f);
+    if (ctx.flag_read()) {
+      tsqr_release(ctx, f->f);
+      TTB_THROW(TTB_ERR_NUMERIC, "non-finite entries in the TSQR panel");
+    }
   } catch (...) {
     delete f;
     throw;

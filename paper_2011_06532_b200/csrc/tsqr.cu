@@ -308,14 +308,19 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
 }
 
 // sign fix: D = sign(diag R) (0 -> +1), Rout = D R (upper), both device
+// (non-finite entries anywhere in the panel reach R: *bad is set, as
+// local_qr raises NumericError for them, tsqr.py:116-117)
 __global__ void sign_fix_kernel(const double* __restrict__ R, int b, double* __restrict__ D,
-                                double* __restrict__ Rout) {
+                                double* __restrict__ Rout, int* __restrict__ bad) {
+  bool finite = true;
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int r = idx % b, k = idx / b;
     const double dr = R[r + b * r] < 0.0 ? -1.0 : 1.0;
     Rout[idx] = (r <= k) ? dr * R[idx] : 0.0;
+    if (r <= k && !isfinite(R[idx])) finite = false;
     if (k == 0) D[r] = dr;
   }
+  if (!finite) *bad = 1;
 }
 
 // ------------------------------------------------------------------------
@@ -711,7 +716,7 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   } else {
     f.Rraw = f.Rlocal;
   }
-  sign_fix_kernel<<<1, 256, 0, st>>>(f.Rraw, f.b, f.D, f.R);
+  sign_fix_kernel<<<1, 256, 0, st>>>(f.Rraw, f.b, f.D, f.R, ctx.flag());
   TTB_LAUNCHED();
 }
 
