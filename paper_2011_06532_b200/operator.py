@@ -184,7 +184,7 @@ def _halo(comm, slab, plan, send_idx):
     return halo
 
 
-def _spmm(comm, slab, t_op, plan_dev, out, a0, c0):
+def _spmm(comm, slab, plan_dev, out, a0, c0):
     plan, indptr, cols, vals, send_idx = plan_dev
     rl, dloc, rr = slab.shape
     halo = _halo(comm, slab, plan, send_idx)
@@ -195,6 +195,9 @@ def _spmm(comm, slab, t_op, plan_dev, out, a0, c0):
                                   C.c_void_p(out.data_ptr()), out.shape[0], out.shape[1], a0, c0))
 
 
+_MAX_FUSED_TERMS = 16  # ttb_mode2_spmm_sum's term capacity
+
+
 def _apply_terms(op, dt: DistTTTensor) -> DistTTTensor:
     """sum_t (term t applied to dt), assembled block-diagonally in one pass
     per core (equal to add(add(p0, p1), ...) of the reference, ops.py:330-333):
@@ -202,15 +205,29 @@ def _apply_terms(op, dt: DistTTTensor) -> DistTTTensor:
     in its diagonal block and exact zeros elsewhere."""
     comm = dt.comm
     N, T = dt.ndim, len(op.terms)
-    if N == 1 and T > 1:
+    if N == 1 and T > 1:  # one core: the terms add elementwise, left to right
         from .ops import add_n
 
-        return add_n([_apply_terms(KroneckerOperator(op.dims, [f]), dt) for f in op.terms])
+        parts = [_apply_terms(KroneckerOperator(op.dims, [f]), dt) for f in op.terms]
+        acc = add_n(parts[:_MAX_FUSED_TERMS])
+        for k in range(_MAX_FUSED_TERMS, T, _MAX_FUSED_TERMS - 1):
+            acc = add_n([acc] + parts[k:k + _MAX_FUSED_TERMS - 1])
+        return acc
     ranks = (1,) + tuple(T * r for r in dt.ranks[1:-1]) + (1,)
     lib = _lib.load()
     outs = []
     for n, slab in enumerate(dt.local):
         rl, dloc, rr = slab.shape
+        if T > _MAX_FUSED_TERMS:  # zero-filled core, one block-writing launch per term
+            import torch
+
+            shape = (ranks[n], dloc, ranks[n + 1])
+            o = torch.zeros(shape[0] * shape[1] * shape[2], dtype=torch.float64, device=comm.device)
+            o = o.as_strided(shape, (1, shape[0], shape[0] * shape[1]))
+            for t in range(T):
+                _spmm(comm, slab, _dev_plan(op, t, n, comm), o, 0 if n == 0 else t * rl, 0 if n == N - 1 else t * rr)
+            outs.append(o)
+            continue
         o = f_empty(ranks[n], dloc, ranks[n + 1], comm.device)
         plans = [_dev_plan(op, t, n, comm) for t in range(T)]
         halos = [_halo(comm, slab, pd[0], pd[4]) for pd in plans]  # exchanges (P > 1), in term order
@@ -260,7 +277,7 @@ def mode2_multiply(core, a):
     slab = to_device_slab(arr, comm.device)
     op = KroneckerOperator((d,), [[a]])
     out = f_empty(rl, d, rr, comm.device)
-    _spmm(comm, slab, op.terms[0][0], _dev_plan(op, 0, 0, comm), out, 0, 0)
+    _spmm(comm, slab, _dev_plan(op, 0, 0, comm), out, 0, 0)
     return TTCore(to_host_array(out)) if host else out
 
 

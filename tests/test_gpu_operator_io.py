@@ -159,6 +159,21 @@ def test_apply_operator_serial_bitwise():
     bitwise(cores_of(ident), tt("op_x"))
 
 
+def test_apply_operator_many_terms():
+    """More terms than the fused one-pass kernel takes (16): per-term launches."""
+    dims = (5, 4, 6)
+    x = O.random_cores(dims, (1, 2, 2, 1), 40)
+    rng = np.random.default_rng(41)
+    terms = [[sp.random(d, d, density=0.5, random_state=int(rng.integers(1 << 30)), format="csr") for d in dims]
+             for _ in range(18)]
+    op = T.KroneckerOperator(dims, terms)
+    z = T.apply_operator(op, T.TTTensor(x))
+    bitwise(cores_of(z), O.apply_operator(op.terms, x))
+    x1 = O.random_cores((7,), (1, 1), 42)
+    op1 = T.KroneckerOperator((7,), [[sp.random(7, 7, density=0.5, random_state=k, format="csr")] for k in range(20)])
+    bitwise(cores_of(T.apply_operator(op1, T.TTTensor(x1))), O.apply_operator(op1.terms, x1))
+
+
 def test_apply_operator_device_tensor_and_dims_check():
     x = T.TTTensor(tt("op_x"))
     op = T.KroneckerOperator((6, 5, 7), kron_sum_terms((6, 5, 7)))
