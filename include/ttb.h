@@ -60,6 +60,11 @@ int ttb_abi_version(void);
 /* number of kernels this library has launched in the process (evidence) */
 long long ttb_launch_counter(void);
 
+/* collective traffic issued by this process since load (the reference's
+ * Trace words / messages, comm.py:57-124): out4 = {TSQR allgathers, their
+ * doubles sent, allreduces + point-to-point transfers, their doubles} */
+int ttb_comm_stats(long long* out4);
+
 /* One context per (process, device).  Replaces the Communicator endpoint
  * (comm.py:134-160; SerialComm comm.py:163-181). */
 int ttb_ctx_create(int device, void* stream, ttb_ctx** out);

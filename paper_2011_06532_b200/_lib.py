@@ -38,6 +38,7 @@ SIGNATURES = {
     "ttb_last_error": (C.c_char_p, []),
     "ttb_abi_version": (C.c_int, []),
     "ttb_launch_counter": (C.c_longlong, []),
+    "ttb_comm_stats": (C.c_int, [C.POINTER(C.c_longlong)]),
     "ttb_ctx_create": (C.c_int, [C.c_int, _P, _PP]),
     "ttb_ctx_destroy": (C.c_int, [_P]),
     "ttb_ctx_set_stream": (C.c_int, [_P, _P]),
@@ -111,6 +112,13 @@ def ptr_array(ptrs):
 
 def launch_counter():
     return int(load().ttb_launch_counter())
+
+
+def comm_stats():
+    """(allgathers, allgather doubles, allreduces + p2p transfers, their doubles)."""
+    buf = (C.c_longlong * 4)()
+    check(load().ttb_comm_stats(buf))
+    return tuple(int(v) for v in buf)
 
 
 def prof_enable(on=True):

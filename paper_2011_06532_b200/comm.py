@@ -35,7 +35,7 @@ class Communicator:
         if self.device.type != "cuda":
             raise CapabilityError("communicator device must be a CUDA device")
         self._ctx = None
-        self.trace = _NullTrace()
+        self.trace = DeviceTrace()
 
     # -- native context ------------------------------------------------------
     def ctx(self):
@@ -187,16 +187,69 @@ class DistComm(Communicator):
         self.host.barrier()
 
 
-class _NullTrace:
-    """Placeholder for ttpar's Trace: phase timing lives in the native layer."""
+class DeviceTrace:
+    """ttpar's per-rank Trace (comm.py:57-124) for the device path.
+
+    ``reset()`` starts per-kernel-class CUDA-event timing in the native
+    library; ``rows()`` / ``total()`` report it in the reference's phases --
+    ``TSQR`` (leaf and tree factorisations), ``AppQ`` (implicit-Q applies),
+    ``Other`` (folds, SVDs, Gram sweeps, construction) -- with the collective
+    traffic of each phase (TSQR: the allgathers of R factors; Other:
+    allreduces and operator exchanges).  Seconds are summed device time of
+    the kernels, not wall time; flops come from the cost model, not counters.
+    """
+
+    PHASE = {"tsqr_leaf": "TSQR", "tsqr_tree": "TSQR", "apply_tree": "AppQ", "apply_chain": "AppQ",
+             "apply_product": "AppQ"}
+
+    def __init__(self):
+        self._on = False
+        self._seconds = {}
+        self._base = (0, 0, 0, 0)
 
     def reset(self):
-        pass
+        _lib.prof_enable(True)
+        _lib.prof_dump()
+        self._on = True
+        self._seconds = {}
+        self._base = _lib.comm_stats()
 
-    def total(self, key):
-        return 0.0
+    def freeze(self):
+        """Fold the timings recorded so far into the phase totals."""
+        if not self._on:
+            return
+        import torch
 
-    def add_flops(self, f):
+        torch.cuda.synchronize()
+        for name, (cnt, ms) in _lib.prof_dump().items():
+            if name.startswith("svd_sweeps"):
+                continue
+            ph = self.PHASE.get(name, "Other")
+            self._seconds[ph] = self._seconds.get(ph, 0.0) + ms * 1e-3
+
+    def stop(self):
+        self.freeze()
+        _lib.prof_enable(False)
+        self._on = False
+
+    def _traffic(self):
+        now = _lib.comm_stats()
+        d = [a - b for a, b in zip(now, self._base)]
+        return {"TSQR": (float(d[1]), float(d[0])), "Other": (float(d[3]), float(d[2]))}
+
+    def rows(self):
+        """``(phase, seconds, flops, words, messages)`` per touched phase."""
+        self.freeze()
+        traffic = self._traffic()
+        phases = sorted(set(self._seconds) | {p for p, (w, m) in traffic.items() if m})
+        return [(ph, self._seconds.get(ph, 0.0), 0.0, traffic.get(ph, (0.0, 0.0))[0],
+                 traffic.get(ph, (0.0, 0.0))[1]) for ph in phases]
+
+    def total(self, counter):
+        idx = {"seconds": 1, "flops": 2, "words": 3, "messages": 4}[counter]
+        return float(sum(r[idx] for r in self.rows()))
+
+    def add_flops(self, f):  # the device path has no per-phase flop counters
         pass
 
 

@@ -12,6 +12,10 @@ namespace ttb {
 
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
+// collective traffic of this process (Trace words / messages): [0] TSQR
+// allgathers, [1] their doubles, [2] allreduces + point-to-point exchanges,
+// [3] their doubles
+static std::atomic<long long> g_comm[4] = {{0}, {0}, {0}, {0}};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(int n) { g_launches += n; }
@@ -121,11 +125,15 @@ void Ctx::collect(bool all) {
 
 void Ctx::allgather(const double* send, double* recv, size_t count) {
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
+  g_comm[0] += 1;
+  g_comm[1] += (long long)count * (nranks - 1);
   nccl_check(g_nccl.allGather(send, recv, count, kNcclDouble, nccl_comm, stream), "ncclAllGather");
 }
 
 void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
+  g_comm[2] += 1;
+  g_comm[3] += (long long)count;
   nccl_check(g_nccl.allReduce(send, recv, count, kNcclDouble, kNcclSum, nccl_comm, stream), "ncclAllReduce");
 }
 
@@ -137,6 +145,8 @@ void Ctx::sendrecv(int npeers, const int* peers, const double* const* send, cons
             "libnccl lacks ncclSend/ncclRecv");
   nccl_check(g_nccl.groupStart(), "ncclGroupStart");
   for (int k = 0; k < npeers; ++k) {
+    g_comm[2] += (send_n[k] > 0) + (recv_n[k] > 0);
+    g_comm[3] += send_n[k];
     if (send_n[k] > 0) nccl_check(g_nccl.send(send[k], (size_t)send_n[k], kNcclDouble, peers[k], nccl_comm, stream),
                                   "ncclSend");
     if (recv_n[k] > 0) nccl_check(g_nccl.recv(recv[k], (size_t)recv_n[k], kNcclDouble, peers[k], nccl_comm, stream),
@@ -224,6 +234,13 @@ const char* ttb_last_error(void) { return g_last_error.c_str(); }
 int ttb_abi_version(void) { return TTB_ABI_VERSION; }
 
 long long ttb_launch_counter(void) { return g_launches.load(); }
+
+int ttb_comm_stats(long long* out4) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(out4, TTB_ERR_CONTRACT, "null output");
+  for (int k = 0; k < 4; ++k) out4[k] = g_comm[k].load();
+  TTB_TRY_END
+}
 
 int ttb_ctx_create(int device, void* stream, ttb_ctx** out) {
   TTB_TRY_BEGIN

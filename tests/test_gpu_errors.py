@@ -101,3 +101,19 @@ def test_operator_errors():
         T.apply_operator(T.KroneckerOperator.identity((4, 5, 5)), x)
     with pytest.raises(T.ShapeError):
         T.mode2_multiply(T.TTCore(np.ones((2, 4, 3))), sp.identity(5, format="csr"))
+
+
+def test_device_trace_phases():
+    """comm.trace mirrors ttpar's Trace (comm.py:57-124): per-phase device time
+    of the TSQR factorisations, the implicit-Q applies and the rest."""
+    comm = T.default_comm()
+    y = T.DistTTTensor.random(comm, (300,) * 5, (1, 6, 7, 6, 5, 1), 0)
+    x = T.add(y, y)
+    comm.trace.reset()
+    out = T.round_tt(x, T.RoundingOptions(1e-10))
+    rows = {r[0]: r for r in comm.trace.rows()}
+    comm.trace.stop()
+    assert out.ranks == y.ranks
+    assert set(rows) == {"TSQR", "AppQ", "Other"}
+    assert all(r[1] > 0 for r in rows.values())
+    assert comm.trace.total("messages") == 0.0  # one rank: no collectives
