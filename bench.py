@@ -263,7 +263,8 @@ def run_ours(args):
     peak_hbm, peak_src = hbm_peak()
     roofline = {"bound": "fp64", "kernel": "tsqr_leaf (Householder TSQR leaf chains)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": leaf_traffic(), "peak_source": "measured fp64 (ttb_fp64_peak: DFMA %.1f, DMMA %.1f TF/s)" % (dfma, dmma),
+                "traffic": (leaf_traffic() or {}).get("bytes_per_launch"), "traffic_detail": leaf_traffic(),
+                "peak_source": "measured fp64 (ttb_fp64_peak: DFMA %.1f, DMMA %.1f TF/s)" % (dfma, dmma),
                 "launches": leaf_launch, "ms_per_step": leaf_ms,
                 "share_of_step": leaf_ms / ms if ms else None}
     step_roofline = {"hbm_frac": value / peak_hbm, "hbm_peak_gbs": peak_hbm, "hbm_peak_source": peak_src,
