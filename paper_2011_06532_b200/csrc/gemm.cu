@@ -122,7 +122,13 @@ constexpr int kFoldMinB = TTB_FOLD_MINB;  // resident CTAs per SM
 
 __device__ __forceinline__ unsigned fd_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArgs a) {
+// RIGHT = false: B = H, one contiguous K x J block per chunk (ld K).
+// RIGHT = true:  B(k, j) = V[j + Mb k] (the right fold V R^T): a chunk is K
+//                runs of J doubles, one bulk copy each, staged k-major with a
+//                padded row (ldB = 4 mod 16: conflict-free B fragments).
+template <bool RIGHT, int J>
+__global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) {
+  constexpr int kFoldJ = J;  // columns per chunk
   extern __shared__ __align__(128) double fsm[];
   constexpr int NW = kFoldNT / 32;
   const int M = a.M, K = a.K;
@@ -135,7 +141,8 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
   double* Ss = fsm + 16;                          // MP x ldS (row m)
   double* Bs = Ss + (int64_t)MP * ldS;            // stages of K x kFoldJ
   Bs += (16 - ((Bs - fsm) & 15)) & 15;
-  const int64_t bstage = (int64_t)K * kFoldJ;
+  constexpr int ldB = kFoldJ + 4;                 // RIGHT: row stride of a stage
+  const int64_t bstage = RIGHT ? (int64_t)K * ldB : (int64_t)K * kFoldJ;
   if (tid < kFoldStages) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fd_smem(&bar[tid])) : "memory");
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   for (int idx = tid; idx < MP * ldS; idx += kFoldNT) {
@@ -145,16 +152,29 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
   const int64_t nch = (N + kFoldJ - 1) / kFoldJ;
   __syncthreads();
   auto issue = [&](int64_t c, int st) {
-    if (tid != 0) return;
     const int64_t j0 = c * kFoldJ;
     const int nj = (int)min64(kFoldJ, N - j0);
     const unsigned bytes = (unsigned)(K * nj * 8);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     fd_smem(Bs + st * bstage)),
-                 "l"(a.B + K * j0), "r"(bytes), "r"(fd_smem(&bar[st]))
-                 : "memory");
+    if constexpr (!RIGHT) {
+      if (tid != 0) return;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       fd_smem(Bs + st * bstage)),
+                   "l"(a.B + K * j0), "r"(bytes), "r"(fd_smem(&bar[st]))
+                   : "memory");
+    } else {
+      if (tid >= 32) return;
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
+                     : "memory");
+      __syncwarp();
+      for (int k = tid; k < K; k += 32)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         fd_smem(Bs + st * bstage + (int64_t)k * ldB)),
+                     "l"(a.B + j0 + a.bsk * k), "r"((unsigned)(nj * 8)), "r"(fd_smem(&bar[st]))
+                     : "memory");
+    }
   };
   int st = 0, ph = 0, fill = 0;
   for (int64_t c = blockIdx.x; c < nch && fill < kFoldStages; c += gridDim.x, ++fill) issue(c, fill);
@@ -179,8 +199,10 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       const bool c0 = n0 + fr < nj, c1 = n0 + 8 + fr < nj;
-      const double* b0p = bs + (int64_t)K * (n0 + fr);
-      const double* b1p = bs + (int64_t)K * (n0 + 8 + fr);
+      // B(k, n): left Bs[k + K n], right Bs[n + ldB k]
+      const double* b0p = RIGHT ? bs + (n0 + fr) : bs + (int64_t)K * (n0 + fr);
+      const double* b1p = RIGHT ? bs + (n0 + 8 + fr) : bs + (int64_t)K * (n0 + 8 + fr);
+      constexpr int bks = RIGHT ? ldB : 1;
       const double* a0p = Ss + (int64_t)(m0 + fr) * ldS;
       const double* a1p = Ss + (int64_t)(m0 + 8 + fr) * ldS;
       // upper-triangular S (the R-fold, dtrmm): rows m0.. have no entries left of column m0
@@ -189,8 +211,8 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
         const int k = k0 + fc;
         const bool kin = k < K;
         const double a0 = a0p[k], a1 = a1p[k];  // zero padded
-        const double b0 = (c0 && kin) ? b0p[k] : 0.0;
-        const double b1 = (c1 && kin) ? b1p[k] : 0.0;
+        const double b0 = (c0 && kin) ? b0p[k * bks] : 0.0;
+        const double b1 = (c1 && kin) ? b1p[k * bks] : 0.0;
         dmma_884(acc[0][0][0], acc[0][0][1], a0, b0);
         dmma_884(acc[0][1][0], acc[0][1][1], a0, b1);
         dmma_884(acc[1][0][0], acc[1][0][1], a1, b0);
@@ -203,7 +225,10 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int m = m0 + 8 * i + fr, n = n0 + 8 * jj + 2 * fc + h;
-            if (m < M && n < nj) a.O[m + (int64_t)M * (j0 + n)] = acc[i][jj][h];
+            if (m < M && n < nj) {
+              if constexpr (RIGHT) a.O[m * a.osm + (j0 + n)] = acc[i][jj][h];
+              else a.O[m + (int64_t)M * (j0 + n)] = acc[i][jj][h];
+            }
           }
     }
     __syncthreads();  // stage st consumed
@@ -219,20 +244,26 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_left_kernel(SkinnyArg
   }
 }
 
-static bool fold_left_tma(Ctx& ctx, const SkinnyArgs& a) {
-  // bulk copies need 16-byte sizes / addresses: K * columns even, aligned base
-  if (a.K % 2 != 0 || ((uintptr_t)a.B & 15) || a.N < (int64_t)kFoldJ * ctx.num_sms) return false;  // (enough chunks for every SM)
+template <bool RIGHT, int J>
+static bool fold_tma(Ctx& ctx, const SkinnyArgs& a) {
+  constexpr int kFoldJ = J;
+  // bulk copies need 16-byte sizes / addresses: K * columns (left) or the
+  // row count and leading dimension (right) even, aligned base
+  if (((uintptr_t)a.B & 15) || a.N < (int64_t)kFoldJ * ctx.num_sms) return false;  // (enough chunks for every SM)
+  if (!RIGHT && a.K % 2 != 0) return false;
+  if (RIGHT && ((a.N % 2) || (a.bsk % 2) || a.bsj != 1)) return false;
   const int ldS = ((a.K + 11) & ~15) + 4, MP = (a.M + 15) & ~15;
-  const size_t smem = (16 + (size_t)MP * ldS + 16 + (size_t)kFoldStages * a.K * kFoldJ) * sizeof(double);
+  const size_t bst = RIGHT ? (size_t)a.K * (kFoldJ + 4) : (size_t)a.K * kFoldJ;
+  const size_t smem = (16 + (size_t)MP * ldS + 16 + (size_t)kFoldStages * bst) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(fold_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TTB_CUDA(cudaFuncSetAttribute(fold_kernel<RIGHT, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   if (smem * kFoldMinB > 227 * 1024) return false;
   const int64_t nch = (a.N + kFoldJ - 1) / kFoldJ;
   const int grid = (int)std::min<int64_t>(nch, (int64_t)kFoldMinB * ctx.num_sms);
-  fold_left_kernel<<<grid, kFoldNT, smem, ctx.stream>>>(a);
+  fold_kernel<RIGHT, J><<<grid, kFoldNT, smem, ctx.stream>>>(a);
   TTB_LAUNCHED();
   return true;
 }
@@ -255,7 +286,7 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
   a.osm = 1;
   a.osj = M;
   a.upper = upper ? 1 : 0;
-  if (getenv("TTB_FOLD_V1") == nullptr && fold_left_tma(ctx, a)) return;
+  if (getenv("TTB_FOLD_V1") == nullptr && fold_tma<false, 64>(ctx, a)) return;
   launch_skinny(ctx, a);
 }
 
@@ -277,6 +308,8 @@ void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, cons
   a.osm = Mb;
   a.osj = 1;
   a.upper = upper ? 1 : 0;  // S = G^T: upper triangular when G is lower (V R^T)
+  // right fold: K runs per chunk -- wider chunks for small K keep each copy >= 2 KB
+  if (getenv("TTB_FOLD_V1") == nullptr && (K <= 16 ? fold_tma<true, 256>(ctx, a) : fold_tma<true, 64>(ctx, a))) return;
   launch_skinny(ctx, a);
 }
 
