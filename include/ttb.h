@@ -126,6 +126,12 @@ int ttb_sumsq(ttb_ctx* ctx, int64_t n, const double* x, double* result);
 int ttb_orthonormalize(ttb_ctx* ctx, int direction, int ndim, const int64_t* dims,
                        const int64_t* ranks, const double* const* in, double* const* out);
 
+/* ||x||^2 by the orthonormalization route (norm(method="ortho"),
+ * ops.py:208-235): a right-to-left sweep of TSQR R factors folded into the
+ * next core, without forming the orthonormal cores; *result on the host. */
+int ttb_norm_ortho(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* ranks, const double* const* in,
+                   double* result);
+
 /* round_tt (parallel.py:293-438) with RoundingOptions (parallel.py:261-284).
  * variant: 0 LRLI, 1 LRL, 2 RLRI, 3 RLR.  max_rank <= 0 means no cap.
  * out[n] sized by the input ranks; results packed at the front with shape

@@ -53,6 +53,7 @@ SIGNATURES = {
     "ttb_inner": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PD]),
     "ttb_sumsq": (C.c_int, [_P, _I64, _P, _PD]),
     "ttb_orthonormalize": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PP]),
+    "ttb_norm_ortho": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PP, _PD]),
     "ttb_round": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PP, _PP, _PI64, _PD]),
     "ttb_round_host": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PP, _PP, _PI64, _PD]),
     "ttb_tsqr_factor": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _PP, _P]),

@@ -244,6 +244,44 @@ int ttb_orthonormalize(ttb_ctx* h, int direction, int ndim, const int64_t* dims,
   TTB_TRY_END
 }
 
+// ||x||^2 by the orthonormalization route (ops.py:208-235, method "ortho"):
+// a right-to-left sweep of R factors only -- TSQR of H(work_n)^T, fold R
+// into core n-1 -- without forming the orthonormal cores (no implicit-Q
+// apply, no output writes); ||x|| = ||work_0||_F.
+int ttb_norm_ortho(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* ranks, const double* const* in,
+                   double* result) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, ranks);
+  TTB_CHECK(result, TTB_ERR_CONTRACT, "null result");
+  const int N = ndim;
+  if (N == 1) {
+    *result = global_sumsq(ctx, ranks[0] * dims[0] * ranks[1], in[0]);
+    return TTB_OK;
+  }
+  int64_t maxc = 1;
+  for (int n = 0; n < N - 1; ++n) maxc = std::max<int64_t>(maxc, ranks[n] * dims[n] * ranks[n + 1]);
+  double* buf[2] = {(double*)ctx.alloc((size_t)maxc * sizeof(double)),
+                    (double*)ctx.alloc((size_t)maxc * sizeof(double))};
+  ctx.flag_reset();
+  const double* work = in[N - 1];
+  int which = 0;
+  for (int n = N - 1; n >= 1; --n) {
+    const int b = (int)ranks[n];
+    Tsqr f;
+    tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 1), f);
+    gemm_small_right(ctx, ranks[n - 1] * dims[n - 1], b, b, in[n - 1], f.R, b, true, buf[which], true);
+    tsqr_release(ctx, f);
+    work = buf[which];
+    which ^= 1;
+  }
+  TTB_CHECK(!ctx.flag_read(), TTB_ERR_NUMERIC, "non-finite entries in the tensor (orthonormalization)");
+  *result = global_sumsq(ctx, ranks[0] * dims[0] * ranks[1], work);
+  ctx.free(buf[0]);
+  ctx.free(buf[1]);
+  TTB_TRY_END
+}
+
 // Host-resident cores for ttb_round_host: the H2D copy of every input core
 // is queued up front on the context's copy stream (one event per core) and
 // the compute stream waits for core n only where the sweep first reads it;

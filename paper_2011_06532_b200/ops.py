@@ -150,20 +150,15 @@ def inner_product(x, y) -> float:
     return float(res.value)
 
 
-def _sumsq(comm, slab):
-    lib = _lib.load()
-    res = C.c_double(0.0)
-    _lib.check(lib.ttb_sumsq(comm.ctx(), slab.numel(), C.c_void_p(slab.data_ptr()), C.byref(res)))
-    return float(res.value)
-
-
 def norm(x, method: str = "innerprod", return_info: bool = False):
     """Frobenius norm by one of three routes (ops.py:208-235).
 
     ``innerprod``: sqrt(<x, x>) with the fused Gram kernel.
     ``innerprod_sym``: the same Gram sweep (the device kernel already fuses
-    both products; it never falls back).  ``ortho``: right-orthonormalize a
-    copy and read the norm off core 0 (no cancellation floor).
+    both products; it never falls back).  ``ortho``: the R factors of a
+    right-to-left orthonormalization folded core by core, the norm read off
+    the last folded core (no cancellation floor; the orthonormal cores are
+    never formed).
     """
     if method not in NORM_METHODS:
         raise ContractError(f"unknown norm method {method!r}; pick from {NORM_METHODS}")
@@ -171,9 +166,10 @@ def norm(x, method: str = "innerprod", return_info: bool = False):
     dx, _ = _as_dist(x)
     if method in ("innerprod", "innerprod_sym"):
         val = sqrt(max(inner_product(dx, dx), 0.0))
-    else:
-        from .parallel import orthonormalize
-
-        o = orthonormalize(dx, "right")
-        val = sqrt(max(_sumsq(dx.comm, o.local[0]), 0.0))
+    else:  # R factors of a right-to-left orthonormalization, folded (ttb_norm_ortho)
+        lib = _lib.load()
+        res = C.c_double(0.0)
+        _lib.check(lib.ttb_norm_ortho(dx.comm.ctx(), dx.ndim, _lib.i64_array(dx.local_dims()),
+                                      _lib.i64_array(dx.ranks), _ptrs(dx.local), C.byref(res)))
+        val = sqrt(max(float(res.value), 0.0))
     return (val, info) if return_info else val
