@@ -117,6 +117,22 @@ int ttb_fill_random(ttb_ctx* ctx, const uint32_t* seed, int nseed, int nslabs, c
 int ttb_inner(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* rx, const int64_t* ry,
               const double* const* x, const double* const* y, double* result);
 
+/* ||x||^2 by the symmetric Gram route (norm(method="innerprod_sym"),
+ * ops.py:179-205): per mode a rank-revealing pivoted Cholesky of the carry
+ * W = (P L)(P L)^T, then W' = Z^T Z with Z = (P L)^T H(x_n), allreduced.
+ * *indefinite = 1 when a carry fails the reconstruction check (ops.py:173-
+ * 175); *result is then unspecified and the caller falls back to
+ * ttb_inner, as ops.py:226-230 does. */
+int ttb_norm_sym(ttb_ctx* ctx, int ndim, const int64_t* dims, const int64_t* ranks, const double* const* in,
+                 double* result, int* indefinite);
+
+/* _pivoted_cholesky (ops.py:162-176) of a device n x n SPSD matrix w
+ * (n <= 64, lower triangle read): pl (device n x n) = P L in w's row order,
+ * zero columns past the numeric rank (pivot <= 1e-14 max diag); perm (host,
+ * n ints) = the pivots in order, then the remaining rows; *indefinite = 1
+ * when ||pl pl^T - w||_F > 1e-6 ||w||_F. */
+int ttb_pivoted_cholesky(ttb_ctx* ctx, int n, const double* w, double* pl, int* perm, int* rank, int* indefinite);
+
 /* sum of squares of n doubles, allreduced (parallel.py:362-365, ops.py:232-234) */
 int ttb_sumsq(ttb_ctx* ctx, int64_t n, const double* x, double* result);
 

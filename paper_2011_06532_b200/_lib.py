@@ -52,6 +52,9 @@ SIGNATURES = {
                                   _PI64, _PP]),
     "ttb_inner": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PD]),
     "ttb_sumsq": (C.c_int, [_P, _I64, _P, _PD]),
+    "ttb_norm_sym": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PP, _PD, C.POINTER(C.c_int)]),
+    "ttb_pivoted_cholesky": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int)]),
     "ttb_orthonormalize": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PP]),
     "ttb_norm_ortho": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PP, _PD]),
     "ttb_round": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PP, _PP, _PI64, _PD]),

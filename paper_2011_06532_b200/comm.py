@@ -205,6 +205,7 @@ class DeviceTrace:
     def __init__(self):
         self._on = False
         self._seconds = {}
+        self._flops = {}
         self._base = (0, 0, 0, 0)
 
     def reset(self):
@@ -212,6 +213,7 @@ class DeviceTrace:
         _lib.prof_dump()
         self._on = True
         self._seconds = {}
+        self._flops = {}
         self._base = _lib.comm_stats()
 
     def freeze(self):
@@ -241,16 +243,19 @@ class DeviceTrace:
         """``(phase, seconds, flops, words, messages)`` per touched phase."""
         self.freeze()
         traffic = self._traffic()
-        phases = sorted(set(self._seconds) | {p for p, (w, m) in traffic.items() if m})
-        return [(ph, self._seconds.get(ph, 0.0), 0.0, traffic.get(ph, (0.0, 0.0))[0],
+        phases = sorted(set(self._seconds) | set(self._flops) | {p for p, (w, m) in traffic.items() if m})
+        return [(ph, self._seconds.get(ph, 0.0), self._flops.get(ph, 0.0), traffic.get(ph, (0.0, 0.0))[0],
                  traffic.get(ph, (0.0, 0.0))[1]) for ph in phases]
 
     def total(self, counter):
         idx = {"seconds": 1, "flops": 2, "words": 3, "messages": 4}[counter]
         return float(sum(r[idx] for r in self.rows()))
 
-    def add_flops(self, f):  # the device path has no per-phase flop counters
-        pass
+    def add_flops(self, f, phase="Other"):
+        """Cost-model flops of a host-issued operation (the reference's
+        tr.add_flops calls, e.g. ops.py:151, 193-201); counted while tracing."""
+        if self._on:
+            self._flops[phase] = self._flops.get(phase, 0.0) + float(f)
 
 
 _default = {}

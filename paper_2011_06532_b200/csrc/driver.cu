@@ -195,6 +195,72 @@ int ttb_inner(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* rx, cons
   TTB_TRY_END
 }
 
+// ||x||^2 by the symmetric Gram route (norm(method="innerprod_sym"),
+// ops.py:179-205): per mode a pivoted Cholesky of the carry, Z = (P L)^T
+// H(x_n), W = Z^T Z, allreduced.  An indefinite carry (reconstruction
+// residual above 1e-6 ||W||_F at any mode) sets *indefinite and leaves
+// *result unspecified: the caller falls back to ttb_inner (ops.py:226-230).
+int ttb_norm_sym(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* ranks, const double* const* in,
+                 double* result, int* indefinite) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  check_chain(ndim, dims, ranks);
+  TTB_CHECK(result && indefinite, TTB_ERR_CONTRACT, "null result");
+  for (int n = 0; n <= ndim; ++n) TTB_CHECK(ranks[n] <= 64, TTB_ERR_CAPABILITY, "norm: ranks above 64");
+  double* buf = (double*)ctx.alloc(5 * 64 * 64 * sizeof(double) + 72 * sizeof(int));
+  double* W = buf;
+  double* Wn = buf + 4096;
+  double* Wr = buf + 8192;
+  double* PL = buf + 12288;
+  double* Wrec = buf + 16384;
+  int* perm = (int*)(buf + 20480);
+  int* ticket = perm + 64;
+  static const double one = 1.0;
+  TTB_CUDA(cudaMemcpyAsync(W, &one, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+  TTB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), ctx.stream));
+  ctx.flag_reset();
+  pivoted_cholesky(ctx, W, 1, PL, Wrec, perm, nullptr);
+  for (int n = 0; n < ndim; ++n) {
+    const bool last = n == ndim - 1;
+    // one rank: the 16 x 16 step factors the next carry in its own tail
+    if (!last && ctx.nranks == 1 && sym16_fusable(ranks[n], ranks[n + 1], dims[n], in[n])) {
+      gram_sym_step(ctx, PL, perm, Wrec, in[n], ranks[n], ranks[n + 1], dims[n], nullptr, ticket);
+      continue;
+    }
+    gram_sym_step(ctx, PL, perm, Wrec, in[n], ranks[n], ranks[n + 1], dims[n], Wn, nullptr);
+    if (ctx.nranks > 1) {
+      ctx.allreduce_sum(Wn, Wr, (size_t)(ranks[n + 1] * ranks[n + 1]));
+      std::swap(Wn, Wr);
+    }
+    std::swap(W, Wn);
+    if (!last) pivoted_cholesky(ctx, W, (int)ranks[n + 1], PL, Wrec, perm, nullptr);
+  }
+  *result = host_scalar(ctx, W);
+  *indefinite = ctx.flag_read() ? 1 : 0;
+  ctx.free(buf);
+  TTB_TRY_END
+}
+
+// the reference's _pivoted_cholesky (ops.py:162-176) on one device carry:
+// w and pl are device n x n (col-major); pl = P L in w's row order with zero
+// columns past the numeric rank; perm (host, n ints) lists the pivots first.
+int ttb_pivoted_cholesky(ttb_ctx* h, int n, const double* w, double* pl, int* perm, int* rank, int* indefinite) {
+  TTB_TRY_BEGIN
+  Ctx& ctx = h->c;
+  TTB_CHECK(w && pl && perm && rank && indefinite, TTB_ERR_CONTRACT, "null argument");
+  int* ints = (int*)ctx.alloc(72 * sizeof(int));
+  ctx.flag_reset();
+  pivoted_cholesky(ctx, w, n, pl, nullptr, ints, ints + 64);
+  int hbuf[65];
+  TTB_CUDA(cudaMemcpyAsync(hbuf, ints, 65 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  TTB_CUDA(cudaStreamSynchronize(ctx.stream));
+  for (int i = 0; i < n; ++i) perm[i] = hbuf[i];
+  *rank = hbuf[64];
+  *indefinite = ctx.flag_read() ? 1 : 0;
+  ctx.free(ints);
+  TTB_TRY_END
+}
+
 int ttb_sumsq(ttb_ctx* h, int64_t n, const double* x, double* result) {
   TTB_TRY_BEGIN
   *result = global_sumsq(h->c, n, x);

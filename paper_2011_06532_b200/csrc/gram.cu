@@ -331,6 +331,164 @@ __global__ void __launch_bounds__(NT, 1) gram2_kernel(Gram2Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// innerprod_sym (ops.py:158-205): the Gram carry is factored W = (P L)(P L)^T
+// by a rank-revealing pivoted Cholesky (dpstrf's greedy largest-remaining-
+// diagonal pivoting, stop when the pivot is not above 1e-14 * max diag W) and
+// the recurrence carries Z = (P L)^T H(x_n), W' = Z^T Z.  The (n <= 64)
+// carry is read from its lower triangle, as dpstrf(lower=1) does, one
+// element per thread (registers), with no row swaps: column j of P L is
+// written in the carry's own row order, and (P L)(P L)^T accumulates
+// alongside for the reconstruction check -- a residual above 1e-6 ||W||_F
+// (ops.py:173-175) sets the context flag and the caller falls back to the
+// plain inner product.
+// ---------------------------------------------------------------------------
+constexpr double kPstrfRtol = 1e-14;
+constexpr double kGramResidRtol = 1e-6;
+
+struct PcholSmem {
+  double diag[64], colp[64], red[2][16];
+  int chosen[64], order[64];
+  int p, rank;
+  double piv, tol;
+};
+
+// W: n x n (col-major, generic pointer, lower triangle read).  Outputs (any
+// may be null): PL (n x n), Wrec = (P L)(P L)^T, perm (pivots then the rest),
+// rank; *flag = 1 on an indefinite carry.
+template <int NT, int NMAX>
+__device__ void pchol_dev(const double* W, int n, double* PL, double* Wrec, int* perm, int* rank_out, int* flag,
+                          PcholSmem& S) {
+  constexpr int Q = (NMAX * NMAX + NT - 1) / NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nn = n * n;
+  double a[Q], rec[Q], w0[Q];
+  int ii[Q], kk[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int e = tid + NT * q;
+    ii[q] = e < nn ? e % n : -1;
+    kk[q] = e < nn ? e / n : -1;
+    a[q] = e < nn ? W[max(ii[q], kk[q]) + n * min(ii[q], kk[q])] : 0.0;
+    w0[q] = a[q];
+    rec[q] = 0.0;
+    if (e < nn && ii[q] == kk[q]) S.diag[ii[q]] = a[q];
+  }
+  for (int i = tid; i < 64; i += NT) S.chosen[i] = 0;
+  __syncthreads();
+  if (warp == 0) {
+    double m = -INFINITY;
+    for (int i = lane; i < n; i += 32) m = fmax(m, S.diag[i]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      S.tol = kPstrfRtol * fmax(m, 0.0);
+      S.rank = n;
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    if (j > 0) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (ii[q] >= 0 && ii[q] == kk[q]) S.diag[ii[q]] = S.chosen[ii[q]] ? -INFINITY : a[q];
+    }
+    __syncthreads();
+    if (warp == 0) {  // the largest remaining diagonal, lowest index on ties
+      double v = -INFINITY;
+      int p = n;
+      for (int i = lane; i < n; i += 32) {
+        const double d = S.diag[i];
+        if (d > v) {
+          v = d;
+          p = i;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (ov > v || (ov == v && op < p)) {
+          v = ov;
+          p = op;
+        }
+      }
+      if (lane == 0) {
+        S.p = p;
+        S.piv = v;
+      }
+    }
+    __syncthreads();
+    const double piv = S.piv;
+    if (!(piv > S.tol)) {  // numeric rank reached (NaN pivots stop too)
+      if (tid == 0) S.rank = j;
+      break;
+    }
+    const int p = S.p;
+    const double d = sqrt(piv), rd = 1.0 / d;  // dpstrf scales by the reciprocal
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (kk[q] == p) {
+        const int i = ii[q];
+        const double v = i == p ? d : (S.chosen[i] ? 0.0 : a[q] * rd);
+        S.colp[i] = v;
+        if (PL) PL[i + n * j] = v;
+      }
+    if (tid == 0) {
+      S.chosen[p] = 1;
+      S.order[j] = p;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (ii[q] >= 0) {
+        const double ci = S.colp[ii[q]], ck = S.colp[kk[q]];
+        rec[q] = fma(ci, ck, rec[q]);
+        if (!S.chosen[ii[q]] && !S.chosen[kk[q]]) a[q] = fma(-ci, ck, a[q]);
+      }
+  }
+  __syncthreads();
+  const int rank = S.rank;
+  double r2 = 0.0, w2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (ii[q] >= 0) {
+      r2 += (rec[q] - w0[q]) * (rec[q] - w0[q]);
+      w2 += w0[q] * w0[q];
+      if (Wrec) Wrec[ii[q] + n * kk[q]] = rec[q];
+      if (PL && kk[q] >= rank) PL[ii[q] + n * kk[q]] = 0.0;
+    }
+  for (int o = 16; o; o >>= 1) {
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+  }
+  if (lane == 0) {
+    S.red[0][warp] = r2;
+    S.red[1][warp] = w2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double R2 = 0.0, W2 = 0.0;
+    for (int w = 0; w < NT / 32; ++w) {
+      R2 += S.red[0][w];
+      W2 += S.red[1][w];
+    }
+    if (!(sqrt(R2) <= kGramResidRtol * fmax(sqrt(W2), 1e-300))) *flag = 1;
+    if (rank_out) *rank_out = rank;
+    if (perm) {
+      int q = rank;
+      for (int i = 0; i < rank; ++i) perm[i] = S.order[i];
+      for (int i = 0; i < n; ++i)
+        if (!S.chosen[i]) perm[q++] = i;
+    }
+  }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(256) pchol_kernel(const double* __restrict__ W, int n, double* __restrict__ PL,
+                                                    double* __restrict__ Wrec, int* __restrict__ perm,
+                                                    int* __restrict__ rank_out, int* __restrict__ flag) {
+  __shared__ PcholSmem S;
+  pchol_dev<256, NMAX>(W, n, PL, Wrec, perm, rank_out, flag, S);
+}
+
+// ---------------------------------------------------------------------------
 // Rank-16 specialisation (every rank 16: the interior cores of BASELINE
 // cfg2) on the m16n8k8 fp64 MMA: a whole 16 x 16 Z^T and accumulator per
 // warp, W^T fragments held in registers for the whole launch, 8 MMAs and 12
@@ -366,40 +524,79 @@ __device__ __forceinline__ void dmma1688(double (&d)[4], double a0, double a1, d
       : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
 }
 
+// SYM (the innerprod_sym route, ops.py:179-205): W holds P L, the carry's
+// pivoted Cholesky factor in the carry's row order (16 x 16, zero columns
+// past the numeric rank) and Y is unused; Z^T = H(X)^T M^T as
+// above, then acc = Z^T Z with the same D fragments serving as the A operand
+// (M = d, K = c: a = {z0, z2, z1, z3}) -- one operand stream instead of two.
+// The contraction index a runs in pivot order (perm), where P L is lower
+// triangular: the zero (a < 8, c >= 8) block of Z^T's first product is
+// skipped, and of the symmetric Z^T Z only the (d, b < 8) m16n8 tile and the
+// (d, b >= 8) m8n8 block are formed (the rest is their mirror): 6 instead of
+// 8 m16n8k8-equivalents per slice.
+__device__ __forceinline__ void dmma884(double (&d)[4], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+template <bool SYM>
 __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restrict__ W, const double* __restrict__ X,
-                                                           const double* __restrict__ Y, int64_t I, int64_t per_cta,
-                                                           double* __restrict__ part) {
+                                                           const double* __restrict__ Y, const int* __restrict__ perm,
+                                                           int64_t I, int64_t per_cta, double* __restrict__ part,
+                                                           int* __restrict__ ticket, double* __restrict__ Wrec,
+                                                           int* __restrict__ flag) {
+  // SYM streams one operand: twice the slices per chunk in the same stage
+  // bytes, so every warp has a pair of slices per chunk (overlapped chains)
+  constexpr int NS = SYM ? 2 * kG16NS : kG16NS;
+  constexpr int LDX = 16 * NS + 4;
+  constexpr int STAGE = SYM ? 16 * LDX : kG16Stage;
+  static_assert(STAGE <= kG16Stage, "SYM stage must fit the launch's shared memory");
   extern __shared__ __align__(128) double g16[];
   constexpr int NW = kG16NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(g16);
-  double* St = g16 + 16;  // stages: X block (16 x kG16Ldx), then Y block (16 x kG16Ldy)
+  double* St = g16 + 16;  // stages: X block (16 x LDX), then Y block (16 x kG16Ldy)
   if (tid < kG16Stages) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g2_smem(&bar[tid])) : "memory");
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   // W^T B fragments: (k = a, n = c) -> W(c, a) = W[c + 16 a]
   double wf[2][2][2];
+  int pa[2][2] = {{0, 4}, {8, 12}};
+  if constexpr (SYM) {
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      pa[ks][0] = perm[8 * ks + t];
+      pa[ks][1] = perm[8 * ks + t + 4];
+    }
+  }
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      wf[ks][nt][0] = W[(8 * nt + g) + 16 * (8 * ks + t)];
-      wf[ks][nt][1] = W[(8 * nt + g) + 16 * (8 * ks + t + 4)];
+      if constexpr (SYM) {  // W = P L (carry rows, col-major); a in pivot order
+        wf[ks][nt][0] = W[pa[ks][0] + 16 * (8 * nt + g)];
+        wf[ks][nt][1] = W[pa[ks][1] + 16 * (8 * nt + g)];
+      } else {
+        wf[ks][nt][0] = W[(8 * nt + g) + 16 * (8 * ks + t)];
+        wf[ks][nt][1] = W[(8 * nt + g) + 16 * (8 * ks + t + 4)];
+      }
     }
   const int64_t s_begin = (int64_t)blockIdx.x * per_cta;
   const int64_t s_end = min64(I, s_begin + per_cta);
-  const int nch = s_end > s_begin ? (int)((s_end - s_begin + kG16NS - 1) / kG16NS) : 0;
+  const int nch = s_end > s_begin ? (int)((s_end - s_begin + NS - 1) / NS) : 0;
   __syncthreads();
   auto issue = [&](int c, int st) {  // warp 0: one bulk copy per right index of X and of Y
     if (warp != 0) return;
-    const int64_t i0 = s_begin + (int64_t)c * kG16NS;
-    const int nn = (int)min64(kG16NS, s_end - i0);
+    const int64_t i0 = s_begin + (int64_t)c * NS;
+    const int nn = (int)min64(NS, s_end - i0);
     const unsigned bytes = (unsigned)(16 * nn * 8);
-    if (lane == 0) g2_expect(&bar[st], 32 * bytes);
+    if (lane == 0) g2_expect(&bar[st], (SYM ? 16 : 32) * bytes);
     __syncwarp();
-    double* xs = St + (int64_t)st * kG16Stage;
-    double* ys = xs + 16 * kG16Ldx;
-    if (lane < 16) g2_bulk(xs + (int64_t)lane * kG16Ldx, X + 16 * (i0 + I * lane), bytes, &bar[st]);
+    double* xs = St + (int64_t)st * STAGE;
+    double* ys = xs + 16 * LDX;
+    if (SYM && lane >= 16) return;
+    if (lane < 16) g2_bulk(xs + (int64_t)lane * LDX, X + 16 * (i0 + I * lane), bytes, &bar[st]);
     else g2_bulk(ys + (int64_t)(lane - 16) * kG16Ldy, Y + 16 * (i0 + I * (lane - 16)), bytes, &bar[st]);
   };
   for (int c = 0; c < kG16Stages && c < nch; ++c) issue(c, c);
@@ -411,11 +608,11 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[u][bt][q] = 0.0;
   for (int c = 0, st = 0, ph = 0; c < nch; ++c) {
-    const int64_t i0 = s_begin + (int64_t)c * kG16NS;
-    const int nn = (int)min64(kG16NS, s_end - i0);
+    const int64_t i0 = s_begin + (int64_t)c * NS;
+    const int nn = (int)min64(NS, s_end - i0);
     g2_wait(&bar[st], ph);
-    const double* xs = St + (int64_t)st * kG16Stage;
-    const double* ys = xs + 16 * kG16Ldx;
+    const double* xs = St + (int64_t)st * STAGE;
+    const double* ys = xs + 16 * LDX;
     // slices in pairs: both Z^T first, then both accumulations (two
     // accumulator sets: independent MMA chains the scheduler can overlap)
     auto zt = [&](int ii, double (&z)[2][4]) {  // Z^T (16 x 16): M = b, N = c, K = a
@@ -426,14 +623,24 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
         for (int q = 0; q < 4; ++q) z[nt][q] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        const int a = 8 * ks + t;
-        const double a0 = xp[(int64_t)g * kG16Ldx + a], a1 = xp[(int64_t)(g + 8) * kG16Ldx + a];
-        const double a2 = xp[(int64_t)g * kG16Ldx + a + 4], a3 = xp[(int64_t)(g + 8) * kG16Ldx + a + 4];
+        const int a = SYM ? pa[ks][0] : 8 * ks + t, a4 = SYM ? pa[ks][1] : 8 * ks + t + 4;
+        const double a0 = xp[(int64_t)g * LDX + a], a1 = xp[(int64_t)(g + 8) * LDX + a];
+        const double a2 = xp[(int64_t)g * LDX + a4], a3 = xp[(int64_t)(g + 8) * LDX + a4];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma1688(z[nt], a0, a1, a2, a3, wf[ks][nt][0], wf[ks][nt][1]);
+        for (int nt = 0; nt < 2; ++nt)
+          if (!SYM || nt <= ks) dmma1688(z[nt], a0, a1, a2, a3, wf[ks][nt][0], wf[ks][nt][1]);
       }
     };
     auto accum = [&](int ii, const double (&z)[2][4], double (&ac)[2][4]) {  // acc(d, b) += Y(c, d) Z(c, b)
+      if constexpr (SYM) {
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          dmma1688(ac[0], z[kc][0], z[kc][2], z[kc][1], z[kc][3], z[kc][0], z[kc][1]);
+          dmma884(ac[1], z[kc][2], z[kc][2]);  // (d, b >= 8) block, k = c = 8 kc + 2 t
+          dmma884(ac[1], z[kc][3], z[kc][3]);  //                     k = c = 8 kc + 2 t + 1
+        }
+        return;
+      }
       const double* yp = ys + 16 * ii;
 #pragma unroll
       for (int kc = 0; kc < 2; ++kc) {
@@ -463,6 +670,17 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
   }
   // per-warp 16 x 16 partials, summed over warps in a fixed order
   double* red = St;  // NW x 256
+  if constexpr (SYM) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = g + 8 * (q >> 1), b = 2 * t + (q & 1);
+      const double v = acc[0][0][q] + acc[1][0][q];
+      red[warp * 256 + d + 16 * b] = v;
+      if (q >= 2) red[warp * 256 + b + 16 * d] = v;  // mirror
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) red[warp * 256 + (8 + g) + 16 * (8 + 2 * t + h)] = acc[0][1][h] + acc[1][1][h];
+  } else
 #pragma unroll
   for (int bt = 0; bt < 2; ++bt)
 #pragma unroll
@@ -476,11 +694,39 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
     for (int w = 0; w < NW; ++w) sum += red[w * 256 + e];
     part[(int64_t)blockIdx.x * 256 + e] = sum;
   }
+  if constexpr (SYM) {
+    // with a ticket, the last CTA to finish sums the partials (fixed order)
+    // and factors the new carry in place: P L and perm for the next mode
+    // (every CTA read them before its main loop), no extra launches
+    if (ticket == nullptr) return;
+    __shared__ PcholSmem S;
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double* Wsm = St;  // 3 x 256 (the reduction scratch is free again)
+    {
+      const int e = tid & 255, h = tid >> 8;
+      double s0 = 0.0;
+#pragma unroll 16
+      for (int p = h; p < (int)gridDim.x; p += 2) s0 += __ldcg(part + (int64_t)p * 256 + e);
+      Wsm[256 + tid] = s0;
+    }
+    __syncthreads();
+    if (tid < 256) Wsm[tid] = Wsm[256 + tid] + Wsm[512 + tid];
+    __syncthreads();
+    pchol_dev<kG16NT, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
+    if (tid == 0) *ticket = 0;
+  }
 }
 
 __global__ void gram_final_kernel(const double* __restrict__ part, int nparts, int cnt, double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += blockDim.x * gridDim.x) {
     double s = 0.0;
+#pragma unroll 16
     for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * cnt + e];
     out[e] = s;
   }
@@ -505,11 +751,12 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
     double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
     static bool attr = false;
     if (!attr) {
-      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = true;
     }
     ProfScope ps("gram", ctx.stream);
-    gram16_kernel<<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, I, per_cta, part);
+    gram16_kernel<false><<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, nullptr, I, per_cta, part, nullptr, nullptr,
+                                                             nullptr);
     TTB_LAUNCHED();
     gram_final_kernel<<<1, 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
     TTB_LAUNCHED();
@@ -607,6 +854,56 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
   gram_final_kernel<<<(int)std::max<int64_t>(1, (cnt + 255) / 256), 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
   TTB_LAUNCHED();
   ctx.free(part);
+}
+
+
+void pivoted_cholesky(Ctx& ctx, const double* W, int n, double* PL, double* Wrec, int* perm, int* rank) {
+  TTB_CHECK(n >= 1 && n <= 64, TTB_ERR_CAPABILITY, "pivoted Cholesky: carry above 64 x 64");
+  ProfScope ps("pchol", ctx.stream);
+  auto kern = n <= 16 ? pchol_kernel<16> : n <= 32 ? pchol_kernel<32> : pchol_kernel<64>;
+  kern<<<1, 256, 0, ctx.stream>>>(W, n, PL, Wrec, perm, rank, ctx.flag());
+  TTB_LAUNCHED();
+}
+
+// W' = Z^T Z, Z = (P L)^T H(X); X is (ral, I, rar).  Bond ranks 16 run the
+// fused single-stream kernel; other shapes contract the reconstructed carry
+// (P L)(P L)^T with the two-operand Gram kernels (same value, the flops of
+// innerprod).  With a ticket (16 x 16 only; see sym16_fusable) the step
+// also factors W' in place -- PL, perm, Wrec, the flag -- and Wn is not
+// written.
+bool sym16_fusable(int64_t ral, int64_t rar, int64_t I, const double* X) {
+  static const bool no16 = getenv("TTB_GRAM_NO16") != nullptr;
+  return I > 0 && ral == 16 && rar == 16 && (uintptr_t)X % 16 == 0 && !no16;
+}
+
+void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* X, int64_t ral, int64_t rar,
+                   int64_t I, double* Wn, int* ticket) {
+  if (sym16_fusable(ral, rar, I, X)) {
+    const size_t smem = (16 + (size_t)kG16Stages * kG16Stage) * sizeof(double);
+    constexpr int ns = 2 * kG16NS;
+    int grid = (int)std::min<int64_t>((int64_t)ctx.num_sms, (I + ns - 1) / ns);
+    int64_t per_cta = (I + grid - 1) / grid;
+    per_cta = (per_cta + ns - 1) / ns * ns;
+    grid = (int)((I + per_cta - 1) / per_cta);
+    double* part = (double*)ctx.alloc((size_t)grid * 256 * sizeof(double));
+    static bool attr = false;
+    if (!attr) {
+      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    ProfScope ps("gram", ctx.stream);
+    gram16_kernel<true><<<grid, kG16NT, smem, ctx.stream>>>(PL, X, nullptr, perm, I, per_cta, part, ticket, Wrec,
+                                                            ctx.flag());
+    TTB_LAUNCHED();
+    if (!ticket) {
+      gram_final_kernel<<<1, 256, 0, ctx.stream>>>(part, grid, 256, Wn);
+      TTB_LAUNCHED();
+    }
+    ctx.free(part);
+    return;
+  }
+  TTB_CHECK(!ticket, TTB_ERR_CONTRACT, "fused carry factorization needs 16 x 16 bonds");
+  gram_step(ctx, Wrec, X, ral, rar, X, ral, rar, I, Wn);
 }
 
 }  // namespace ttb

@@ -10,11 +10,12 @@ the reference API); DistTTTensor stays on the device.
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 from math import sqrt
 
 from . import _lib
 from .comm import default_comm
-from .errors import CapacityError, ContractError, ShapeError
+from .errors import CapacityError, ContractError, NumericError, ShapeError
 from .tensor import DistTTTensor, TTTensor, f_empty, to_host_array
 
 NORM_METHODS = ("innerprod", "innerprod_sym", "ortho")
@@ -145,17 +146,62 @@ def inner_product(x, y) -> float:
     dx, dy, _ = _check_pair(x, y)
     lib = _lib.load()
     res = C.c_double(0.0)
-    _lib.check(lib.ttb_inner(dx.comm.ctx(), dx.ndim, _lib.i64_array(dx.local_dims()), _lib.i64_array(dx.ranks),
+    ldims = dx.local_dims()
+    _lib.check(lib.ttb_inner(dx.comm.ctx(), dx.ndim, _lib.i64_array(ldims), _lib.i64_array(dx.ranks),
                              _lib.i64_array(dy.ranks), _ptrs(dx.local), _ptrs(dy.local), C.byref(res)))
+    xr, yr = dx.ranks, dy.ranks
+    dx.comm.trace.add_flops(sum(2.0 * yr[n] * xr[n] * d * xr[n + 1] + 2.0 * yr[n + 1] * yr[n] * d * xr[n + 1]
+                                for n, d in enumerate(ldims)))
     return float(res.value)
+
+
+def _sym_norm(dx):
+    """(||x||, ok) by the symmetric Gram route on the device (ttb_norm_sym;
+    ops.py:179-205).  ok is False when a carry is indefinite."""
+    lib = _lib.load()
+    res, bad = C.c_double(0.0), C.c_int(0)
+    ldims = dx.local_dims()
+    _lib.check(lib.ttb_norm_sym(dx.comm.ctx(), dx.ndim, _lib.i64_array(ldims), _lib.i64_array(dx.ranks),
+                                _ptrs(dx.local), C.byref(res), C.byref(bad)))
+    r = dx.ranks
+    dx.comm.trace.add_flops(sum(float(r[n]) * r[n] * d * r[n + 1] + float(r[n + 1]) * r[n + 1] * r[n] * d
+                                for n, d in enumerate(ldims)))
+    return sqrt(max(float(res.value), 0.0)), not bad.value
+
+
+def pivoted_cholesky(w):
+    """The reference's _pivoted_cholesky (ops.py:162-176) on the device:
+    (lfac, perm, rank) with lfac = (P L)[perm][:, :rank] so that
+    pl[perm] = lfac reconstructs w = pl pl^T.  Raises NumericError on an
+    indefinite w (the reference raises _IndefiniteGram)."""
+    import numpy as np
+    import torch
+
+    comm = default_comm()
+    w = np.asarray(w, dtype=np.float64)
+    n = w.shape[0]
+    if w.shape != (n, n) or n == 0:
+        raise ShapeError(f"expected a square matrix, got {w.shape}")
+    wd = torch.from_numpy(np.asfortranarray(w).ravel(order="F").copy()).to(comm.device)
+    pl = torch.empty(n * n, dtype=torch.float64, device=comm.device)
+    perm = (C.c_int * n)()
+    rank, bad = C.c_int(0), C.c_int(0)
+    _lib.check(_lib.load().ttb_pivoted_cholesky(comm.ctx(), n, C.c_void_p(wd.data_ptr()), C.c_void_p(pl.data_ptr()),
+                                                 perm, C.byref(rank), C.byref(bad)))
+    if bad.value:
+        raise NumericError("Gram carry is not PSD (pivoted Cholesky residual)")
+    p = np.array(perm[:], dtype=int)
+    full = pl.cpu().numpy().reshape((n, n), order="F")
+    return np.asfortranarray(full[p][:, :rank.value]), p, int(rank.value)
 
 
 def norm(x, method: str = "innerprod", return_info: bool = False):
     """Frobenius norm by one of three routes (ops.py:208-235).
 
     ``innerprod``: sqrt(<x, x>) with the fused Gram kernel.
-    ``innerprod_sym``: the same Gram sweep (the device kernel already fuses
-    both products; it never falls back).  ``ortho``: the R factors of a
+    ``innerprod_sym``: a pivoted Cholesky factor of the carry propagated
+    instead of the operand pair (ttb_norm_sym; one operand stream); falls
+    back to ``innerprod`` with a warning when a carry is indefinite.  ``ortho``: the R factors of a
     right-to-left orthonormalization folded core by core, the norm read off
     the last folded core (no cancellation floor; the orthonormal cores are
     never formed).
@@ -164,8 +210,14 @@ def norm(x, method: str = "innerprod", return_info: bool = False):
         raise ContractError(f"unknown norm method {method!r}; pick from {NORM_METHODS}")
     info = {"method": method, "fallback": False}
     dx, _ = _as_dist(x)
-    if method in ("innerprod", "innerprod_sym"):
+    if method == "innerprod":
         val = sqrt(max(inner_product(dx, dx), 0.0))
+    elif method == "innerprod_sym":
+        val, ok = _sym_norm(dx)
+        if not ok:
+            warnings.warn("innerprod_sym fell back to innerprod: indefinite Gram carry", stacklevel=2)
+            info["fallback"] = True
+            val = sqrt(max(inner_product(dx, dx), 0.0))
     else:  # R factors of a right-to-left orthonormalization, folded (ttb_norm_ortho)
         lib = _lib.load()
         res = C.c_double(0.0)
