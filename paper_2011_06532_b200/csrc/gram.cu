@@ -707,16 +707,22 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double* Wsm = St;  // 3 x 256 (the reduction scratch is free again)
+    constexpr int NH = kG16NT / 256;  // threads per carry entry
+    static_assert(kG16NT % 256 == 0, "one or more threads per carry entry");
+    double* Wsm = St;  // (1 + NH) x 256 (the reduction scratch is free again)
     {
       const int e = tid & 255, h = tid >> 8;
       double s0 = 0.0;
 #pragma unroll 16
-      for (int p = h; p < (int)gridDim.x; p += 2) s0 += __ldcg(part + (int64_t)p * 256 + e);
+      for (int p = h; p < (int)gridDim.x; p += NH) s0 += __ldcg(part + (int64_t)p * 256 + e);
       Wsm[256 + tid] = s0;
     }
     __syncthreads();
-    if (tid < 256) Wsm[tid] = Wsm[256 + tid] + Wsm[512 + tid];
+    if (tid < 256) {
+      double w = 0.0;
+      for (int h = 0; h < NH; ++h) w += Wsm[256 * (h + 1) + tid];
+      Wsm[tid] = w;
+    }
     __syncthreads();
     pchol_dev<kG16NT, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
     if (tid == 0) *ticket = 0;
