@@ -57,6 +57,8 @@ def main():
     rows.append(("cfg2 <X,Z>", ms, 2 * bx, cost.gram_flops(dims, r, r)))
     ms, _ = timed(lambda: T.norm(x))
     rows.append(("cfg2 norm (Gram)", ms, bx, cost.gram_flops(dims, r, r)))
+    ms, _ = timed(lambda: T.norm(x, "innerprod_sym"))
+    rows.append(("cfg2 norm (innerprod_sym: pivoted-Cholesky Gram)", ms, bx, cost.gram_flops(dims, r, r) / 2))
     ms, _ = timed(lambda: T.norm(x, "ortho"), reps=3)
     rows.append(("cfg2 norm (ortho: R-factor sweep)", ms, bx, None))
     for direction in ("left", "right"):
