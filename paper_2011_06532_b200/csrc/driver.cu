@@ -176,14 +176,16 @@ int ttb_inner(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* rx, cons
   Ctx& ctx = h->c;
   check_chain(ndim, dims, rx);
   check_chain(ndim, dims, ry);
-  double* buf = (double*)ctx.alloc(3 * 64 * 64 * sizeof(double));
+  double* buf = (double*)ctx.alloc(3 * 64 * 64 * sizeof(double) + 8 * sizeof(int));
   double* W = buf;
   double* Wn = buf + 4096;
   double* Wr = buf + 8192;
+  int* ticket = (int*)(buf + 12288);  // the 16 x 16 kernel's last-CTA reduction
   static const double one = 1.0;
   TTB_CUDA(cudaMemcpyAsync(W, &one, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+  TTB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), ctx.stream));
   for (int n = 0; n < ndim; ++n) {
-    gram_step(ctx, W, x[n], rx[n], rx[n + 1], y[n], ry[n], ry[n + 1], dims[n], Wn);
+    gram_step(ctx, W, x[n], rx[n], rx[n + 1], y[n], ry[n], ry[n + 1], dims[n], Wn, ticket);
     if (ctx.nranks > 1) {
       ctx.allreduce_sum(Wn, Wr, (size_t)(rx[n + 1] * ry[n + 1]));
       std::swap(Wn, Wr);

@@ -694,12 +694,12 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
     for (int w = 0; w < NW; ++w) sum += red[w * 256 + e];
     part[(int64_t)blockIdx.x * 256 + e] = sum;
   }
-  if constexpr (SYM) {
+  {
     // with a ticket, the last CTA to finish sums the partials (fixed order)
-    // and factors the new carry in place: P L and perm for the next mode
-    // (every CTA read them before its main loop), no extra launches
+    // and writes W' to Wrec -- or, SYM, factors it in place: P L and perm
+    // for the next mode (every CTA read them before its main loop) -- so no
+    // second launch sits between two modes
     if (ticket == nullptr) return;
-    __shared__ PcholSmem S;
     __shared__ int s_last;
     __threadfence();
     __syncthreads();
@@ -724,7 +724,12 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
       Wsm[tid] = w;
     }
     __syncthreads();
-    pchol_dev<kG16NT, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
+    if constexpr (SYM) {
+      __shared__ PcholSmem S;
+      pchol_dev<kG16NT, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
+    } else {
+      if (tid < 256) Wrec[tid] = Wsm[tid];
+    }
     if (tid == 0) *ticket = 0;
   }
 }
@@ -739,7 +744,7 @@ __global__ void gram_final_kernel(const double* __restrict__ part, int nparts, i
 }
 
 void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t rar, const double* Y, int64_t rbl,
-               int64_t rbr, int64_t I, double* Wn) {
+               int64_t rbr, int64_t I, double* Wn, int* ticket) {
   TTB_CHECK(ral <= 64 && rar <= 64 && rbl <= 64 && rbr <= 64, TTB_ERR_CAPABILITY, "inner product: ranks above 64");
   const int64_t cnt = rbr * rar;
   if (I == 0) {
@@ -761,11 +766,13 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
       attr = true;
     }
     ProfScope ps("gram", ctx.stream);
-    gram16_kernel<false><<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, nullptr, I, per_cta, part, nullptr, nullptr,
+    gram16_kernel<false><<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, nullptr, I, per_cta, part, ticket, Wn,
                                                              nullptr);
     TTB_LAUNCHED();
-    gram_final_kernel<<<1, 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
-    TTB_LAUNCHED();
+    if (!ticket) {
+      gram_final_kernel<<<1, 256, 0, ctx.stream>>>(part, grid, (int)cnt, Wn);
+      TTB_LAUNCHED();
+    }
     ctx.free(part);
     return;
   }

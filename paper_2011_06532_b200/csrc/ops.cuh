@@ -22,7 +22,7 @@ void fill_zero(Ctx& ctx, double* p, int64_t n);
 
 // gram.cu: Wn (rbr x rar) = sum_i Y(i)^T W X(i); W (rbl x ral) device
 void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t rar, const double* Y, int64_t rbl,
-               int64_t rbr, int64_t I, double* Wn);
+               int64_t rbr, int64_t I, double* Wn, int* ticket = nullptr);
 void pivoted_cholesky(Ctx& ctx, const double* W, int n, double* PL, double* Wrec, int* perm, int* rank);
 bool sym16_fusable(int64_t ral, int64_t rar, int64_t I, const double* X);
 void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* X, int64_t ral, int64_t rar,
