@@ -512,6 +512,18 @@ __global__ void __launch_bounds__(256) pchol_kernel(const double* __restrict__ W
 constexpr int kG16NS = TTB_G16_NS;           // slices per chunk
 constexpr int kG16Stages = TTB_G16_STAGES;
 constexpr int kG16NT = TTB_G16_NT;           // warps take the chunk's slices round-robin
+#ifndef TTB_G16S_NT
+#define TTB_G16S_NT 512
+#endif
+#ifndef TTB_G16S_NS
+#define TTB_G16S_NS 32
+#endif
+#ifndef TTB_G16S_CPS
+#define TTB_G16S_CPS 1
+#endif
+constexpr int kG16sNT = TTB_G16S_NT;   // SYM: threads, slices per chunk, CTAs per SM
+constexpr int kG16sNS = TTB_G16S_NS;
+constexpr int kG16sCPS = TTB_G16S_CPS;
 constexpr int kG16Ldx = 16 * kG16NS + 4;     // 4 mod 16: conflict-free scalar A loads
 constexpr int kG16Ldy = 16 * kG16NS + 8;     // 8 mod 16: conflict-free 16-byte A loads
 constexpr int kG16Stage = 16 * kG16Ldx + 16 * kG16Ldy;
@@ -541,19 +553,20 @@ __device__ __forceinline__ void dmma884(double (&d)[4], double a, double b) {
 }
 
 template <bool SYM>
-__global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restrict__ W, const double* __restrict__ X,
+__global__ void __launch_bounds__(SYM ? kG16sNT : kG16NT, SYM ? kG16sCPS : 1) gram16_kernel(const double* __restrict__ W, const double* __restrict__ X,
                                                            const double* __restrict__ Y, const int* __restrict__ perm,
                                                            int64_t I, int64_t per_cta, double* __restrict__ part,
                                                            int* __restrict__ ticket, double* __restrict__ Wrec,
                                                            int* __restrict__ flag) {
   // SYM streams one operand: twice the slices per chunk in the same stage
   // bytes, so every warp has a pair of slices per chunk (overlapped chains)
-  constexpr int NS = SYM ? 2 * kG16NS : kG16NS;
+  constexpr int NS = SYM ? kG16sNS : kG16NS;
   constexpr int LDX = 16 * NS + 4;
   constexpr int STAGE = SYM ? 16 * LDX : kG16Stage;
-  static_assert(STAGE <= kG16Stage, "SYM stage must fit the launch's shared memory");
   extern __shared__ __align__(128) double g16[];
-  constexpr int NW = kG16NT / 32;
+  constexpr int NTK = SYM ? kG16sNT : kG16NT;
+  constexpr int NW = NTK / 32;
+  static_assert(NW * 256 <= kG16Stages * STAGE, "reduction scratch fits the stages");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(g16);
@@ -689,7 +702,7 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
       red[warp * 256 + d + 16 * b] = acc[0][bt][q] + acc[1][bt][q];
     }
   __syncthreads();
-  for (int e = tid; e < 256; e += kG16NT) {
+  for (int e = tid; e < 256; e += NTK) {
     double sum = 0.0;
     for (int w = 0; w < NW; ++w) sum += red[w * 256 + e];
     part[(int64_t)blockIdx.x * 256 + e] = sum;
@@ -707,8 +720,8 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    constexpr int NH = kG16NT / 256;  // threads per carry entry
-    static_assert(kG16NT % 256 == 0, "one or more threads per carry entry");
+    constexpr int NH = NTK / 256;  // threads per carry entry
+    static_assert(NTK % 256 == 0, "one or more threads per carry entry");
     double* Wsm = St;  // (1 + NH) x 256 (the reduction scratch is free again)
     {
       const int e = tid & 255, h = tid >> 8;
@@ -726,7 +739,7 @@ __global__ void __launch_bounds__(kG16NT, 1) gram16_kernel(const double* __restr
     __syncthreads();
     if constexpr (SYM) {
       __shared__ PcholSmem S;
-      pchol_dev<kG16NT, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
+      pchol_dev<NTK, 16>(Wsm, 16, const_cast<double*>(W), Wrec, const_cast<int*>(perm), nullptr, flag, S);
     } else {
       if (tid < 256) Wrec[tid] = Wsm[tid];
     }
@@ -892,9 +905,9 @@ bool sym16_fusable(int64_t ral, int64_t rar, int64_t I, const double* X) {
 void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* X, int64_t ral, int64_t rar,
                    int64_t I, double* Wn, int* ticket) {
   if (sym16_fusable(ral, rar, I, X)) {
-    const size_t smem = (16 + (size_t)kG16Stages * kG16Stage) * sizeof(double);
-    constexpr int ns = 2 * kG16NS;
-    int grid = (int)std::min<int64_t>((int64_t)ctx.num_sms, (I + ns - 1) / ns);
+    const size_t smem = (16 + (size_t)kG16Stages * 16 * (16 * kG16sNS + 4)) * sizeof(double);
+    constexpr int ns = kG16sNS;
+    int grid = (int)std::min<int64_t>((int64_t)ctx.num_sms * kG16sCPS, (I + ns - 1) / ns);
     int64_t per_cta = (I + grid - 1) / grid;
     per_cta = (per_cta + ns - 1) / ns * ns;
     grid = (int)((I + per_cta - 1) / per_cta);
@@ -905,7 +918,7 @@ void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* 
       attr = true;
     }
     ProfScope ps("gram", ctx.stream);
-    gram16_kernel<true><<<grid, kG16NT, smem, ctx.stream>>>(PL, X, nullptr, perm, I, per_cta, part, ticket, Wrec,
+    gram16_kernel<true><<<grid, kG16sNT, smem, ctx.stream>>>(PL, X, nullptr, perm, I, per_cta, part, ticket, Wrec,
                                                             ctx.flag());
     TTB_LAUNCHED();
     if (!ticket) {
