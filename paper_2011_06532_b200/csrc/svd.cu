@@ -28,6 +28,10 @@ constexpr int kSvdNT = 2 * 32 * kGrp;  // half on the A columns (one pair slot p
 constexpr int kSvdMax = 64;
 constexpr int kLd = kSvdMax + 1;  // padded column stride: distinct columns start on distinct banks
 constexpr int kHalf = kSvdNT / 2;
+#ifndef TTB_SVD_DEFLATE
+#define TTB_SVD_DEFLATE 1
+#endif
+constexpr bool kSvdDeflate = TTB_SVD_DEFLATE != 0;
 
 #ifdef TTB_DEBUG_CLK
 static __device__ long long g_sclk[64 * 4];
@@ -43,6 +47,8 @@ struct SvdSmem {
   double rot[2][kSvdMax / 2][2]; // (cs, sn) of each pair of a round (0, 0: none), by round parity
   double sig[kSvdMax];
   int order[kSvdMax];
+  int cmap[kSvdMax];  // tournament slot -> column (>= n: the empty slot)
+  int nact;           // tournament size of the sweep (even)
   int rotated;
   int bad;
   unsigned long long maxoff;  // max over the sweep of ga^2 / (al be) (a non-negative double's bits)
@@ -105,7 +111,6 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   const bool vside = tid >= kHalf;
   const int ltid = vside ? tid - kHalf : tid;
   const int grp = ltid / kGrp, gl = ltid % kGrp;
-  const int npairs = np / 2;
   const double tol = 4.0 * 2.220446049250313e-16 * sqrt((double)m);
   const double tol2 = tol * tol;
   const double noise2 = 2.220446049250313e-16 * 2.220446049250313e-16;
@@ -135,17 +140,47 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     // factors, the kept rank or the discarded-tail sum (rotations that
     // involve one non-negligible column are still applied)
     const double floor2 = fmax(noise2 * nmax, eps * eps * 1e-4 / (double)np);
-    for (int round = 0; round <= np - 1; ++round) {
+    // deflation: from the second sweep on, a column whose norm is at or
+    // below the rotation threshold times the largest (4 eps sqrt(m) ||a||max,
+    // e.g. the roundoff columns of a rank-deficient R) leaves the tournament:
+    // by Weyl, skipping its rotations moves every singular value and factor
+    // by at most its norm, the normwise accuracy LAPACK's gesdd itself has.
+    // The live columns keep their index order; an odd count is padded with
+    // an empty slot
+    if (sweep == 0 || !kSvdDeflate) {
+      for (int c = tid; c < np; c += kSvdNT) sm.cmap[c] = c;
+      if (tid == 0) sm.nact = np;
+    } else if (tid < 32) {
+      int base = 0;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        const int c = c0 + tid;
+        const bool act = c < n && sm.nrm[c] > tol2 * nmax;
+        const unsigned msk = __ballot_sync(0xffffffffu, act);
+        if (act) sm.cmap[base + __popc(msk & ((1u << tid) - 1u))] = c;
+        base += __popc(msk);
+      }
+      if (tid == 0) {
+        if (base & 1) sm.cmap[base] = kSvdMax;
+        sm.nact = base + (base & 1);
+      }
+    }
+    __syncthreads();
+    const int nt = sm.nact, npairs = nt / 2;
+    for (int round = 0; round <= nt - 1; ++round) {
       SVD_CLK(0);
       if (!vside) {
-        if (round < np - 1) {
+        if (round < nt - 1) {
           // one pair slot per group (npairs <= kHalf / kGrp): the whole
           // warp reaches the shuffles together
           const int pr = grp;
           int p = 0, q = 0;
           const bool live = pr < npairs;
-          if (live) pair_of(pr, round, np, p, q);
-          const bool valid = live && q < n;
+          if (live) {
+            pair_of(pr, round, nt, p, q);
+            p = sm.cmap[p];
+            q = sm.cmap[q];
+          }
+          const bool valid = live && p < n && q < n;
           double* ap = sm.A + kLd * p;
           double* aq = sm.A + kLd * q;
           double xa[kSvdMax / kGrp], ya[kSvdMax / kGrp];
@@ -200,7 +235,9 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
           const double cs = sm.rot[rr & 1][pr][0], sn = sm.rot[rr & 1][pr][1];
           if (cs == 0.0) continue;
           int p, q;
-          pair_of(pr, rr, np, p, q);
+          pair_of(pr, rr, nt, p, q);
+          p = sm.cmap[p];
+          q = sm.cmap[q];
           double* vp = sm.V + kLd * p;
           double* vq = sm.V + kLd * q;
           double xv[kSvdMax / kGrp], yv[kSvdMax / kGrp];

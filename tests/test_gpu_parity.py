@@ -160,6 +160,26 @@ def test_truncated_svd_wide_and_random():
         assert np.linalg.norm(a - f.u @ np.diag(f.s) @ f.v.T) <= eps + 1e-12
 
 
+@pytest.mark.parametrize("eps_rel", [0.0, 1e-12, 1e-6])
+def test_truncated_svd_rank_deficient_triangle(eps_rel):
+    # the R factor of an exactly rank-deficient panel (X = Y + Y): half of
+    # its columns are roundoff, which the Jacobi tournament deflates
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal((4000, 30))
+    r = np.linalg.qr(np.hstack([b, b]) @ np.diag(rng.uniform(0.5, 2.0, 60)), mode="r")
+    a = r.T
+    s = np.linalg.svd(a, compute_uv=False)
+    eps = eps_rel * s[0]
+    f = T.truncated_svd(a, eps)
+    tails = [np.sqrt((s[k:] ** 2).sum()) for k in range(s.size + 1)]
+    want = max(next(k for k, tl in enumerate(tails) if tl <= eps), 1)
+    if eps_rel > 0:
+        assert f.s.size == want == 30
+    assert np.allclose(f.s[:30], s[:30], rtol=1e-12)
+    assert np.all(f.s[30:] < 1e-13 * s[0])
+    assert np.linalg.norm(a - f.u @ np.diag(f.s) @ f.v.T) <= eps + 1e-13 * s[0]
+
+
 @pytest.mark.parametrize("direction", ["left", "right"])
 def test_orthonormalize(direction):
     x = tt("orth_in")
