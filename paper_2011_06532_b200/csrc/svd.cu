@@ -140,14 +140,14 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     // factors, the kept rank or the discarded-tail sum (rotations that
     // involve one non-negligible column are still applied)
     const double floor2 = fmax(noise2 * nmax, eps * eps * 1e-4 / (double)np);
-    // deflation: from the second sweep on, a column whose norm is at or
+    // deflation: at every sweep start, a column whose norm is at or
     // below the rotation threshold times the largest (4 eps sqrt(m) ||a||max,
     // e.g. the roundoff columns of a rank-deficient R) leaves the tournament:
     // by Weyl, skipping its rotations moves every singular value and factor
     // by at most its norm, the normwise accuracy LAPACK's gesdd itself has.
     // The live columns keep their index order; an odd count is padded with
     // an empty slot
-    if (sweep == 0 || !kSvdDeflate) {
+    if (!kSvdDeflate) {
       for (int c = tid; c < np; c += kSvdNT) sm.cmap[c] = c;
       if (tid == 0) sm.nact = np;
     } else if (tid < 32) {
