@@ -74,27 +74,8 @@ def main():
         rows.append((name, ms, cost.rounding_bytes(x.dims, x.ranks, out_ranks),
                      cost.rounding_flops(x.dims, x.ranks, out_ranks, opts.variant)))
 
-    # cfg1 / cfg3: X = Y + Y
-    for name, n, d, ry in (("cfg1 round", 2000, 8, 10), ("cfg3 round", 8000, 10, 30)):
-        dims = (n,) * d
-        rk = (1,) + (ry,) * (d - 1) + (1,)
-        y = dev_random(comm, dims, rk, 0)
-        rounding(name, T.add(y, y), T.RoundingOptions(1e-10), rk)
-        del y
-    torch.cuda.empty_cache()
-    T.empty_cache()
-
-    # cfg4: X = 1.0 Y + 0.5 Z - 0.25 Y, dims [2^24, 64^4, 2^20], 60 -> 40
-    dims = (1 << 24, 64, 64, 64, 64, 1 << 20)
-    r = (1,) + (20,) * 5 + (1,)
-    y, z = dev_random(comm, dims, r, 0), dev_random(comm, dims, r, 1)
-    x = T.add_n([y, z, y], [1.0, 0.5, -0.25])
-    del y, z
-    rounding("cfg4 round", x, T.RoundingOptions(1e-8), (1,) + (40,) * 5 + (1,))
-    del x
-    torch.cuda.empty_cache()
-    T.empty_cache()
-
+    # cfg5 first after cfg2: its 16 GB operand and ~40 GB of rounding
+    # workspace measure cleanly before cfg4's 2^24-row panels fragment the pools
     # cfg5: X o W, d=12, n=50000, r=8 -> 64, round(max_rank=32, eps0=0)
     dims, r = (50_000,) * 12, (1,) + (8,) * 11 + (1,)
     x, w = dev_random(comm, dims, r, 0), dev_random(comm, dims, r, 1)
@@ -119,6 +100,27 @@ def main():
     rounding("cfg5 round (cap 32)", p, T.RoundingOptions(0.0, "LRLI", max_rank=32), (1,) + (32,) * 11 + (1,))
 
     del p
+    torch.cuda.empty_cache()
+    T.empty_cache()
+
+    # cfg1 / cfg3: X = Y + Y
+    for name, n, d, ry in (("cfg1 round", 2000, 8, 10), ("cfg3 round", 8000, 10, 30)):
+        dims = (n,) * d
+        rk = (1,) + (ry,) * (d - 1) + (1,)
+        y = dev_random(comm, dims, rk, 0)
+        rounding(name, T.add(y, y), T.RoundingOptions(1e-10), rk)
+        del y
+    torch.cuda.empty_cache()
+    T.empty_cache()
+
+    # cfg4: X = 1.0 Y + 0.5 Z - 0.25 Y, dims [2^24, 64^4, 2^20], 60 -> 40
+    dims = (1 << 24, 64, 64, 64, 64, 1 << 20)
+    r = (1,) + (20,) * 5 + (1,)
+    y, z = dev_random(comm, dims, r, 0), dev_random(comm, dims, r, 1)
+    x = T.add_n([y, z, y], [1.0, 0.5, -0.25])
+    del y, z
+    rounding("cfg4 round", x, T.RoundingOptions(1e-8), (1,) + (40,) * 5 + (1,))
+    del x
     torch.cuda.empty_cache()
     T.empty_cache()
 
