@@ -5,7 +5,8 @@ pipe utilisation (profiles/r1_kernel_roofline.txt is the summary).
     ncu --set full --clock-control none -k regex:'<kernels>' -c 16 -o prof \
         python profiles/kernel_roofline.py                     # capture
 
-Workloads: cfg2 <X,Z> (rank-16 Gram), cfg5-sized Hadamard, one cfg3 rounding
+Workloads: cfg2 <X,Z> (rank-16 Gram) and its innerprod_sym norm, cfg5-sized
+Hadamard, one cfg3 rounding
 (leaf, tree, SVD, fold, apply).  Each is run twice; the capture skips
 nothing, so the first (cold) launch of each kernel is the one recorded.
 """
@@ -22,11 +23,14 @@ import paper_2011_06532_b200 as T  # noqa: E402
 
 def main():
     comm = T.default_comm()
-    dims, r = (100_000,) * 16, (1,) + (16,) * 15 + (1,)
+    # cfg2's interior-core shapes (16 x 100000 x 16), four modes: two interior
+    # launches per kernel keep the capture short
+    dims, r = (100_000,) * 4, (1,) + (16,) * 3 + (1,)
     x, z = T.DistTTTensor.random(comm, dims, r, 0), T.DistTTTensor.random(comm, dims, r, 1)
     T.inner_product(x, z)
+    T.norm(x, "innerprod_sym")
     del x, z
-    dims, r = (50_000,) * 12, (1,) + (8,) * 11 + (1,)
+    dims, r = (50_000,) * 4, (1,) + (8,) * 3 + (1,)  # cfg5's core shapes
     a, w = T.DistTTTensor.random(comm, dims, r, 0), T.DistTTTensor.random(comm, dims, r, 1)
     p = T.hadamard(a, w)
     del a, w, p
