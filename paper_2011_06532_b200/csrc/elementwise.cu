@@ -15,6 +15,10 @@ namespace ttb {
 
 constexpr int kEwNT = 256;
 constexpr int kEwElems = 4096;  // target output elements per CTA
+#ifndef TTB_EW_ELEMS_VEC
+#define TTB_EW_ELEMS_VEC 8192
+#endif
+constexpr int kEwElemsVec = TTB_EW_ELEMS_VEC;  // the paired-row Hadamard path
 
 // Visit the cells (row r, slice ii) of an RL x nn block of an F-order core
 // column, rows fastest so stores coalesce.  mk(r) returns the per-row
@@ -40,6 +44,7 @@ struct AddArgs {
   AddTerm t[kMaxAddTerms];
   int64_t RL, I, RR;
   int ni;  // slices per CTA
+  int vec;  // interior mode with even blocks and aligned cores: paired rows
   double* out;
 };
 
@@ -83,6 +88,20 @@ __global__ void __launch_bounds__(kEwNT) add_kernel(AddArgs a) {
   }
   // interior: block diagonal
   const double* x = T.x + T.rl * (i0 + a.I * (c - T.offc));
+  if (a.vec) {  // even blocks: row pairs never straddle one; 16-byte loads, streaming stores
+    const int RL2 = (int)(RL >> 1), per = kEwNT / RL2;
+    const int r2 = threadIdx.x % RL2, it = threadIdx.x / RL2;
+    if (it >= per) return;
+    const int64_t ai = 2 * r2, al = ai - T.offa;
+    const bool in = al >= 0 && al < T.rl;
+    const double* xr = x + al;
+    const int64_t rl = T.rl;
+    for (int ii = it; ii < ni; ii += per) {
+      const double2 v = in ? *reinterpret_cast<const double2*>(xr + rl * ii) : make_double2(0.0, 0.0);
+      __stcs(reinterpret_cast<double2*>(out + ai + RL * ii), v);
+    }
+    return;
+  }
   for_cells((int)RL, (int)ni, [&](int ai) {
     const int64_t al = ai - T.offa;
     const bool in = al >= 0 && al < T.rl;
@@ -102,7 +121,11 @@ void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, 
   a.RL = RL;
   a.I = I;
   a.RR = RR;
-  a.ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
+  bool vec = mode == 0 && RL % 2 == 0 && RL / 2 <= kEwNT && (uintptr_t)out % 16 == 0;
+  for (int p = 0; p < nterms; ++p)
+    vec = vec && terms[p].rl % 2 == 0 && terms[p].offa % 2 == 0 && (uintptr_t)terms[p].x % 16 == 0;
+  a.vec = vec ? 1 : 0;
+  a.ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, (vec ? kEwElemsVec : kEwElems) / std::max<int64_t>(1, RL)));
   a.out = out;
   TTB_CHECK(RR <= 65535, TTB_ERR_CAPABILITY, "add: output right rank too large");
   dim3 grid((unsigned)((I + a.ni - 1) / a.ni), (unsigned)RR);
@@ -114,7 +137,7 @@ void add_core(Ctx& ctx, int mode, int nterms, const AddTerm* terms, int64_t RL, 
 // Z(a*rbl + c, i, b*rbr + d) = X(a, i, b) * Y(c, i, d)
 __global__ void __launch_bounds__(kEwNT)
 hadamard_kernel(const double* __restrict__ x, int64_t ral, int64_t rar, const double* __restrict__ y, int64_t rbl,
-                int64_t rbr, int64_t I, int ni, int col_fast, double* __restrict__ out) {
+                int64_t rbr, int64_t I, int ni, int col_fast, int vec, double* __restrict__ out) {
   // col_fast: the output column is blockIdx.x, so the CTAs of all columns of
   // a slice run are dispatched together and re-read its input slices from L2
   const int64_t col = col_fast ? blockIdx.x : blockIdx.y;
@@ -126,6 +149,21 @@ hadamard_kernel(const double* __restrict__ x, int64_t ral, int64_t rar, const do
   double* o = out + RL * (i0 + I * col);
   const double* xs = x + ral * (i0 + I * bx);
   const double* ys = y + rbl * (i0 + I * dy);
+  if (vec) {  // row pairs: one 16-byte Y load and one 16-byte streaming store per pair
+    const int RL2 = (int)(RL >> 1), per = kEwNT / RL2;
+    const int r2 = threadIdx.x % RL2, it = threadIdx.x / RL2;
+    if (it >= per) return;
+    const int row = 2 * r2, ax = row / (int)rbl, cy = row - ax * (int)rbl;
+    const double* xp = xs + ax;
+    const double* yp = ys + cy;
+    double* op = o + row;
+    for (int ii = it; ii < nn; ii += per) {
+      const double xv = xp[ral * ii];
+      const double2 yv = *reinterpret_cast<const double2*>(yp + rbl * ii);
+      __stcs(reinterpret_cast<double2*>(op + RL * ii), make_double2(__dmul_rn(xv, yv.x), __dmul_rn(xv, yv.y)));
+    }
+    return;
+  }
   for_cells((int)RL, (int)nn, [&](int row) {
     const int ax = row / (int)rbl, cy = row - ax * (int)rbl;
     const double* xp = xs + ax;
@@ -140,12 +178,17 @@ void hadamard_core(Ctx& ctx, const double* x, int64_t ral, int64_t rar, const do
   const int64_t RL = ral * rbl, RR = rar * rbr;
   if (I == 0) return;
   TTB_CHECK(RR <= 65535 && RL <= (1 << 24), TTB_ERR_CAPABILITY, "hadamard: output rank too large");
-  int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, kEwElems / std::max<int64_t>(1, RL)));
+  // rows in pairs when the pair never straddles a Y column and every pair is
+  // 16-byte aligned (even rbl; aligned bases)
+  const bool vec = rbl % 2 == 0 && RL / 2 <= kEwNT && (uintptr_t)y % 16 == 0 && (uintptr_t)out % 16 == 0;
+  const int64_t elems = vec ? kEwElemsVec : kEwElems;
+  int ni = (int)std::max<int64_t>(1, std::min<int64_t>(I, elems / std::max<int64_t>(1, RL)));
   const int64_t runs = (I + ni - 1) / ni;
   const bool col_fast = runs <= 65535;
   dim3 grid = col_fast ? dim3((unsigned)RR, (unsigned)runs) : dim3((unsigned)runs, (unsigned)RR);
   ProfScope ps("hadamard", ctx.stream);
-  hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, col_fast ? 1 : 0, out);
+  hadamard_kernel<<<grid, kEwNT, 0, ctx.stream>>>(x, ral, rar, y, rbl, rbr, I, ni, col_fast ? 1 : 0, vec ? 1 : 0,
+                                                  out);
   TTB_LAUNCHED();
 }
 
