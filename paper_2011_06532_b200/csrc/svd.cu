@@ -32,6 +32,9 @@ constexpr int kHalf = kSvdNT / 2;
 #define TTB_SVD_DEFLATE 1
 #endif
 constexpr bool kSvdDeflate = TTB_SVD_DEFLATE != 0;
+#ifndef TTB_SVD_STOP
+#define TTB_SVD_STOP 1e-18  // max cos^2 of a sweep below which the next sweep is skipped
+#endif
 
 #ifdef TTB_DEBUG_CLK
 static __device__ long long g_sclk[64 * 4];
@@ -265,7 +268,7 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
     ++sweeps;
     if (!any) break;
 #ifndef TTB_SVD_NO_EARLY_STOP
-    if (maxoff < 1e-18) break;
+    if (maxoff < TTB_SVD_STOP) break;
 #endif
   }
   // singular values
