@@ -33,10 +33,12 @@ def test_norm_sym_matches_oracle(dims, ranks):
     assert val == pytest.approx(O.norm(x, "innerprod"), rel=1e-12)
 
 
-@pytest.mark.parametrize("r", [3, 8])
+@pytest.mark.parametrize("r", [3, 8, 24, 32])
 def test_norm_sym_handles_rank_deficient_gram(r):
     # x + x doubles every bond rank: every carry is exactly singular, the
     # factor drops to the numeric rank without falling back (test_ops.py:201)
+    # r = 24 / 32: carries of 48 / 64 (the generic contraction with the
+    # reconstructed carry, the 64-wide factorization)
     x = O.random_cores((200,) * 5, (1,) + (r,) * 4 + (1,), 20)
     dx = dev(x)
     y = T.add(dx, T.scale(dx, 1.0))
