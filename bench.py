@@ -23,7 +23,7 @@ roofline    = dominant kernel class (TSQR leaf factorization), fp64-bound:
               measured fp64 peak of this device (ttb_fp64_peak)
 cpu_baseline= the CPU restatement of the reference (oracle/, numpy + scipy
               LAPACK, all host threads) on the same X, rank 0 only
---impl reference: that CPU path alone, on a bounded sample of the workload
+--impl reference: that CPU path alone, on the same full workload
 """
 
 from __future__ import annotations
@@ -271,9 +271,17 @@ def run_ours(args):
                      "fp64_frac": (F / (ms * 1e-3) / 1e12) / fp64_peak,
                      "kernel_ms": {k: round(v[1], 3) for k, v in prof.items()}}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_same_input(x, dims, rx, ry, eps0, maxr)
+        o = T.round_tt(x, opts)
+        torch.cuda.synchronize()
+        cpu, parity = cpu_baseline_same_input(x, o, dims, rx, ry, eps0, maxr)
+        del o
+    norms = None
+    if not args.no_norm:
+        del x, y
+        torch.cuda.synchronize()
+        norms = measure_norms(T, comm)
 
     clocks = clk.summary()
     line = {
@@ -300,6 +308,8 @@ def run_ours(args):
         "roofline": roofline,
         "step_roofline": step_roofline,
         "cpu_baseline": cpu,
+        "parity": parity,
+        "norm": norms,
         "clocks": clocks,
     }
     if rank == 0:
@@ -308,23 +318,80 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline_same_input(x, dims, rx, ry, eps0, maxr):
+def threadpool_desc():
+    try:
+        from threadpoolctl import threadpool_info
+        return [{k: d.get(k) for k in ("internal_api", "num_threads", "version")} for d in threadpool_info()]
+    except Exception:
+        return None
+
+
+def cpu_baseline_same_input(x, out, dims, rx, ry, eps0, maxr):
     """The CPU restatement of the reference (oracle/) on the same X, all host
-    threads; one step (~15 s on 8 cores for cfg3)."""
+    threads; one step (~6 s on 16 cores for cfg3).  Its result is also the
+    full-size parity check of the GPU output ``out`` (BASELINE.md section 4
+    step 7): ranks identical, TT-form relative difference by the ortho route,
+    and the norm."""
     from oracle import tt_oracle as O
 
     cores = [np.asfortranarray(s.detach().cpu().numpy()) for s in x.local]
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    out, meta = O.round_tt(cores, eps0, "LRLI", maxr)
+    ref, meta = O.round_tt(cores, eps0, "LRLI", maxr)
     dt = time.perf_counter() - t0
     from paper_2011_06532_b200 import cost
 
     B = cost.rounding_bytes(dims, rx, ry)
-    assert O.ranks_of(out) == tuple(ry)
-    return {"value": B / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"the full workload, 1 step ({dt:.1f} s): oracle.round_tt (numpy+scipy LAPACK/OpenBLAS, "
-                      f"{threads} threads) on the same X copied to host"}
+    got = [np.asfortranarray(s.detach().cpu().numpy()) for s in out.local]
+    rel = O.rel_diff(got, ref)
+    parity = {"ranks_equal": tuple(out.ranks) == O.ranks_of(ref), "rel_err_ortho": rel,
+              "norm_rel": abs(out.meta["norm"] - meta["norm"]) / meta["norm"],
+              "bar": "ranks identical, rel_err_ortho <= 1e-10, norm_rel <= 1e-12",
+              "pass": bool(tuple(out.ranks) == O.ranks_of(ref) and rel <= 1e-10
+                           and abs(out.meta["norm"] - meta["norm"]) <= 1e-12 * meta["norm"])}
+    cpu = {"value": B / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"the full workload, 1 step ({dt:.1f} s): oracle.round_tt (numpy+scipy LAPACK/OpenBLAS, "
+                     f"{threads} threads) on the same X copied to host",
+           "threadpools": threadpool_desc()}
+    return cpu, parity
+
+
+def measure_norms(T, comm, reps=5):
+    """BASELINE's second metric, "norm GB/s": the Gram sweep on cfg2 (d=16,
+    n=100000, ranks 16; X, Z the reference's random_tt seeds 0 / 1, drawn on
+    the device).  GB/s = algorithmic bytes (8 |X| (+ 8 |Z|)) / device time,
+    CUDA events around each call (each returns a host scalar)."""
+    import torch
+
+    from paper_2011_06532_b200 import cost
+
+    dims, r = (100_000,) * 16, (1,) + (16,) * 15 + (1,)
+    x = T.DistTTTensor.random(comm, dims, r, 0)
+    z = T.DistTTTensor.random(comm, dims, r, 1)
+    bx = 8.0 * sum(cost.core_sizes(dims, r))
+    calls = {"inner_xz": (lambda: T.inner_product(x, z), 2 * bx),
+             "norm_innerprod": (lambda: T.norm(x, "innerprod"), bx),
+             "norm_innerprod_sym": (lambda: T.norm(x, "innerprod_sym"), bx),
+             "norm_ortho": (lambda: T.norm(x, "ortho"), bx)}
+    res = {"workload": "cfg2: d=16, n=100000, ranks 16 (X, Z: random_tt seeds 0, 1)", "unit": "GB/s"}
+    stream = torch.cuda.current_stream()
+    for name, (fn, nbytes) in calls.items():
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        res[name] = {"value": nbytes / (ms * 1e-3) / 1e9, "ms": ms, "bytes": nbytes}
+    del x, z
+    torch.cuda.synchronize()
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -340,17 +407,13 @@ def run_reference(args):
     cfg = args.config
     dims, ry, rx = chain(cfg)
     eps0, maxr = CONFIGS[cfg][3], CONFIGS[cfg][4]
-    # bounded sample: shrink the mode size so the whole run stays within ~3 min
-    budget_s = 150.0 / max(1, args.steps + args.warmup)
-    n_full = dims[0]
-    # ~16 s for the full cfg3 rounding on 8 cores; scale by core count
-    est_full = (16.0 * 8.0 / (os.cpu_count() or 8)) if cfg == "cfg3" else 0.5
-    n = int(max(200, min(n_full, n_full * budget_s / max(est_full, 1e-3))))
-    sdims = (n,) * len(dims)
-    y = O.random_cores(sdims, ry, 0) if n * ry[1] ** 2 < 5e7 else None
-    if y is None:
-        rng = np.random.default_rng(0)
-        y = [np.asfortranarray(rng.standard_normal((ry[k], d, ry[k + 1]))) for k, d in enumerate(sdims)]
+    # the full workload (same config as our arm): ~6 s per step on 16 host
+    # cores, so the default --steps/--warmup run takes a few minutes
+    n = dims[0]
+    sdims = dims
+    t0 = time.perf_counter()
+    y = O.random_cores(sdims, ry, 0)
+    t_gen = time.perf_counter() - t0
     x = O.add(y, y)
     times = []
     for it in range(args.warmup + args.steps):
@@ -378,11 +441,13 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (seeded N(0,1) TT cores)",
         "config": {"workload": f"{cfg}: round_tt(X = Y + Y) d={len(dims)} n={dims[0]} ranks {rx[1]}->{ry[1]}, "
-                               f"tol {eps0}, LRLI; CPU sample n={n}", "dims": list(sdims), "in_ranks": list(rx),
-                   "out_ranks": list(ry)},
+                               f"tol {eps0}, LRLI", "dims": list(sdims), "in_ranks": list(rx),
+                   "out_ranks": list(ry), "same_config": True},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"mode size {n} of {n_full} (same d, ranks, tol), oracle.round_tt "
-                                   f"(numpy + scipy LAPACK/OpenBLAS, {threads} threads), mean of {args.steps} steps"},
+                         "sample": f"the full workload (n={n}, same X as our arm: random_tt seed 0, X = Y + Y), "
+                                   f"oracle.round_tt (numpy + scipy LAPACK/OpenBLAS, {threads} threads), "
+                                   f"mean of {args.steps} steps; input generation {t_gen:.1f} s untimed",
+                         "threadpools": threadpool_desc()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -395,7 +460,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (and its parity check)")
+    ap.add_argument("--no-norm", action="store_true", help="skip the cfg2 norm GB/s leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -48,11 +48,14 @@ enum {
   TTB_ERR_CAPACITY = 4,   /* ttpar.errors.CapacityError   */
   TTB_ERR_CUDA = 5,       /* CUDA runtime failure          */
   TTB_ERR_NCCL = 6,       /* NCCL failure                  */
-  TTB_ERR_CAPABILITY = 7  /* ttpar.errors.CapabilityError */
+  TTB_ERR_CAPABILITY = 7, /* ttpar.errors.CapabilityError */
+  TTB_ERR_DEADLOCK = 8    /* ttpar.errors.DeadlockError: a collective
+                             timed out waiting for a peer (comm.py:20-33) */
 };
 
 typedef struct ttb_ctx ttb_ctx;
 typedef struct ttb_tsqr ttb_tsqr;
+typedef struct ttb_group ttb_group;
 
 /* ---- library / context ------------------------------------------------ */
 const char* ttb_last_error(void);
@@ -78,6 +81,24 @@ int ttb_ctx_trim(ttb_ctx* ctx);
  * (replaces MPICommunicator, comm.py:359-401). */
 int ttb_comm_unique_id(void* out128);
 int ttb_ctx_init_comm(ttb_ctx* ctx, int nranks, int rank, const void* id128);
+
+/* In-process group: nranks contexts of ONE process (one host thread per
+ * rank, possibly all on one device) joined into a P-rank group whose
+ * collectives -- the TSQR triangle allgather, the Gram / norm allreduces and
+ * the operator halo exchange -- are stream-ordered device copies with a host
+ * rendezvous instead of NCCL calls, at the same call sites.  The stand-in
+ * for the reference's thread simulator SimComm / run_spmd (comm.py:184-356):
+ * it runs the native multi-rank path (P > 1 R stacks, redundant global
+ * trees, rank-offset applies, allreduced Gram partials) on one GPU.
+ * Reductions are rank-ascending sums.  A rank that fails or waits longer
+ * than TTB_GROUP_TIMEOUT_S (default 300) seconds breaks the group: every
+ * later collective returns TTB_ERR_DEADLOCK. */
+int ttb_group_create(int nranks, ttb_group** out);
+int ttb_group_destroy(ttb_group* grp);
+/* break the group: peers blocked in (or later entering) a collective get
+ * TTB_ERR_DEADLOCK (a rank that failed outside the library calls this) */
+int ttb_group_abort(ttb_group* grp);
+int ttb_ctx_join_group(ttb_ctx* ctx, ttb_group* grp, int rank);
 
 /* ---- construction (no communication) ---------------------------------- */
 /* out = s * x elementwise over n doubles (scale folds into core 0,

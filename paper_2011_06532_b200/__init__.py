@@ -9,7 +9,8 @@ mode-sliced TT tensors, computed by hand-written sm_100a CUDA kernels
 (paper_2011_06532_b200/csrc, C ABI in include/ttb.h).
 """
 
-from .comm import Communicator, DistComm, SerialComm, default_comm, empty_cache
+from .comm import (Communicator, DistComm, LocalComm, LocalGroup, SerialComm, default_comm, empty_cache,
+                   run_local_ranks)
 from .errors import (BoundsError, CapabilityError, CapacityError, ContractError, DeadlockError,
                      NumericError, ShapeError, TTError)
 from .operator import KroneckerOperator, apply_operator, load_operator, mode2_multiply, save_operator
@@ -24,11 +25,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BoundsError", "CapabilityError", "CapacityError", "Communicator", "ContractError", "DeadlockError",
-    "DistComm", "DistTTTensor", "KroneckerOperator", "NumericError", "ROUNDING_VARIANTS", "RoundingOptions", "SerialComm",
+    "DistComm", "DistTTTensor", "KroneckerOperator", "LocalComm", "LocalGroup", "NumericError", "ROUNDING_VARIANTS", "RoundingOptions", "SerialComm",
     "ShapeError", "TSQRFactor", "TTCore", "TTError", "TTTensor", "TruncatedSVD", "add", "add_n",
     "apply_operator", "block_bounds", "default_comm", "distribute", "empty_cache", "gather", "hadamard", "inner_product", "load_operator",
     "load_tt", "load_tt_dist", "mode2_multiply", "norm", "pivoted_cholesky",
-    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "save_operator", "save_tt",
+    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "run_local_ranks", "save_operator", "save_tt",
     "save_tt_dist", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
     "tsqr_factor", "__version__",
 ]

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 import threading
 
-from .errors import (CapabilityError, CapacityError, ContractError, NumericError,
+from .errors import (CapabilityError, CapacityError, ContractError, DeadlockError, NumericError,
                      ShapeError, TTError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -25,6 +25,7 @@ _ERRMAP = {
     5: TTError,        # CUDA runtime failure
     6: TTError,        # NCCL failure
     7: CapabilityError,
+    8: DeadlockError,
 }
 
 _P = C.c_void_p
@@ -45,6 +46,10 @@ SIGNATURES = {
     "ttb_ctx_trim": (C.c_int, [_P]),
     "ttb_comm_unique_id": (C.c_int, [_P]),
     "ttb_ctx_init_comm": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "ttb_group_create": (C.c_int, [C.c_int, _PP]),
+    "ttb_group_destroy": (C.c_int, [_P]),
+    "ttb_group_abort": (C.c_int, [_P]),
+    "ttb_ctx_join_group": (C.c_int, [_P, _P, C.c_int]),
     "ttb_scale": (C.c_int, [_P, _I64, _P, C.c_double, _P]),
     "ttb_add": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PD, _PP]),
     "ttb_hadamard": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PP]),

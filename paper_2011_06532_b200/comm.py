@@ -11,6 +11,7 @@ allreduces) and offers the host-side collectives the harness needs
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -23,6 +24,9 @@ class Communicator:
 
     size = 1
     rank = 0
+    # every rank takes part in every exchange (in-process groups rendezvous
+    # even with an empty peer list; NCCL ranks without peers skip the call)
+    rendezvous = False
 
     def __init__(self, device=None):
         import torch
@@ -80,7 +84,7 @@ class Communicator:
         (ttb_exchange): sends[k] (a float64 tensor or None) goes to
         peers[k], recvs[k] (a float64 tensor view, possibly empty) is filled
         from it.  Stream-ordered on the current stream."""
-        if not peers:
+        if not peers and not self.rendezvous:
             return
         lib = _lib.load()
         ctx = self.ctx()
@@ -88,7 +92,7 @@ class Communicator:
         sn = [0 if t is None else t.numel() for t in sends]
         rp = [t.data_ptr() if t.numel() else 0 for t in recvs]
         rn = [t.numel() for t in recvs]
-        _lib.check(lib.ttb_exchange(ctx, len(peers), (C.c_int * len(peers))(*peers), _lib.ptr_array(sp),
+        _lib.check(lib.ttb_exchange(ctx, len(peers), (C.c_int * max(1, len(peers)))(*peers), _lib.ptr_array(sp),
                                     _lib.i64_array(sn), _lib.ptr_array(rp), _lib.i64_array(rn)))
 
     # -- host-side collectives (harness / gather) ----------------------------
@@ -185,6 +189,131 @@ class DistComm(Communicator):
 
     def barrier(self):
         self.host.barrier()
+
+
+class LocalGroup:
+    """P ranks inside ONE process, one host thread each (ttb_group): the
+    native multi-rank path -- allgathered TSQR triangles and redundant global
+    trees, rank-offset applies, allreduced Gram / norm partials, operator halo
+    exchanges -- runs with stream-ordered device copies and a host rendezvous
+    in place of NCCL, at the same call sites.  The B200 stand-in for the
+    reference's thread simulator (SimComm / run_spmd, comm.py:184-356): it
+    lets one GPU execute the code a P-GPU job executes.  Reductions are
+    rank-ascending sums; a rank that fails breaks the group (DeadlockError
+    for its peers instead of a hang)."""
+
+    def __init__(self, size, timeout=300.0):
+        if size < 1:
+            raise ContractError("group size must be >= 1")
+        self.size = size
+        self.timeout = timeout
+        h = C.c_void_p()
+        _lib.check(_lib.load().ttb_group_create(size, C.byref(h)))
+        self._h = h
+        self._bar = threading.Barrier(size)
+        self._box = [None] * size
+
+    def comm(self, rank, device=None):
+        return LocalComm(self, rank, device)
+
+    def barrier(self):
+        from .errors import DeadlockError
+
+        try:
+            self._bar.wait(self.timeout)
+        except threading.BrokenBarrierError as e:
+            raise DeadlockError("in-process group: a peer failed or timed out") from e
+
+    def abort(self):
+        self._bar.abort()
+        if self._h is not None:
+            _lib.load().ttb_group_abort(self._h)
+
+    def close(self):
+        if self._h is not None:
+            _lib.load().ttb_group_destroy(self._h)
+            self._h = None
+
+
+class LocalComm(Communicator):
+    """Rank ``rank`` of a LocalGroup (ttpar's SimComm endpoint)."""
+
+    rendezvous = True
+
+    def __init__(self, group, rank, device=None):
+        if not 0 <= rank < group.size:
+            raise ContractError(f"rank {rank} outside a group of {group.size}")
+        super().__init__(device)
+        self.group = group
+        self.size = group.size
+        self.rank = rank
+
+    def _init_comm(self):
+        _lib.check(_lib.load().ttb_ctx_join_group(self._ctx, self.group._h, self.rank))
+
+    def allgather_object(self, obj):
+        g = self.group
+        g._box[self.rank] = obj
+        g.barrier()
+        out = list(g._box)
+        g.barrier()
+        return out
+
+    def allreduce_sum(self, arr):
+        out = None
+        for part in self.allgather_object(np.asarray(arr, dtype=np.float64)):  # rank-ascending
+            out = part.copy() if out is None else out + part
+        return out
+
+    def barrier(self):
+        self.group.barrier()
+
+
+def run_local_ranks(size, fn, device=None, timeout=600.0):
+    """Run ``fn(comm)`` for every rank of a fresh ``size``-rank LocalGroup,
+    one host thread and one CUDA stream per rank (the run_spmd analogue,
+    comm.py:338-356); returns the per-rank results in rank order and
+    re-raises the first failure."""
+    import torch
+
+    g = LocalGroup(size)
+    out, err = [None] * size, []
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def run(p):
+        comm = None
+        try:
+            torch.cuda.set_device(dev)
+            s = torch.cuda.Stream(dev)
+            with torch.cuda.stream(s):
+                comm = LocalComm(g, p, dev)
+                out[p] = fn(comm)
+                s.synchronize()
+        except BaseException as e:  # surfaced below
+            err.append((p, e))
+            g.abort()
+        finally:
+            if comm is not None:
+                comm.close()
+
+    th = [threading.Thread(target=run, args=(p,), daemon=True) for p in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    alive = [t for t in th if t.is_alive()]
+    if not alive:
+        g.close()
+    if err:
+        from .errors import DeadlockError
+
+        err.sort(key=lambda pe: isinstance(pe[1], DeadlockError))  # the root cause first
+        raise err[0][1]
+    if alive:
+        from .errors import DeadlockError
+
+        raise DeadlockError(f"{len(alive)} rank thread(s) still running after {timeout} s")
+    return out
 
 
 class DeviceTrace:

@@ -22,6 +22,10 @@ struct Error : public std::runtime_error {
 
 void set_last_error(const std::string& msg);
 void count_launch(int n = 1);
+// raise a kernel's dynamic shared-memory limit on the CURRENT device, once per
+// (kernel, device, size): the attribute is per device, and the bookkeeping is
+// shared by every context / host thread of the process (mutex-guarded)
+void smem_attr(const void* fn, size_t bytes);
 
 #define TTB_THROW(code, msg) throw ::ttb::Error((code), (msg))
 

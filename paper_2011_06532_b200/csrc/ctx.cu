@@ -3,8 +3,11 @@
 
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "ctx.cuh"
 
@@ -19,6 +22,103 @@ static std::atomic<long long> g_comm[4] = {{0}, {0}, {0}, {0}};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(int n) { g_launches += n; }
+
+void smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  TTB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({fn, dev});
+  if (it != done.end() && it->second >= bytes) return;
+  TTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done[{fn, dev}] = bytes;
+}
+
+// ---- in-process group ------------------------------------------------------
+// P contexts of one process (each driven by its own host thread) exchange
+// device buffers at the very call sites NCCL serves in a multi-process run.
+// Every collective is two host rendezvous: (1) every rank posts its send
+// buffers and records a "ready" event on its stream; (2) after copying what
+// it needs (stream-ordered behind the owners' ready events) every rank
+// records "done"; its stream then waits for every peer's done event, so no
+// rank reuses or frees a buffer a peer still reads.  The GPU never waits on
+// an event that was not recorded yet (the rendezvous orders the host calls).
+// Reductions are rank-ascending sums (bitwise deterministic, as the
+// reference's _SimGroup._combine, comm.py:213-227).
+struct LocalGroup {
+  int P;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool broken = false;
+  int joined = 0;
+  std::vector<const void*> post;                  // allgather / allreduce: per rank
+  std::vector<std::pair<const double*, int64_t>> p2p;  // [src * P + dst]
+  std::vector<cudaEvent_t> ready, done;
+  explicit LocalGroup(int p) : P(p), post(p, nullptr), p2p((size_t)p * p, {nullptr, 0}), ready(p, nullptr), done(p, nullptr) {}
+  void barrier() {
+    static const int timeout_s = getenv("TTB_GROUP_TIMEOUT_S") ? atoi(getenv("TTB_GROUP_TIMEOUT_S")) : 300;
+    std::unique_lock<std::mutex> lk(mu);
+    TTB_CHECK(!broken, TTB_ERR_DEADLOCK, "in-process group: a peer failed or timed out");
+    const unsigned long long g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(timeout_s), [&] { return gen != g || broken; })) {
+      broken = true;
+      cv.notify_all();
+      TTB_THROW(TTB_ERR_DEADLOCK, "in-process group: collective timed out waiting for a peer");
+    }
+    TTB_CHECK(gen != g, TTB_ERR_DEADLOCK, "in-process group: a peer failed or timed out");
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
+namespace {
+// a failing rank must release its peers from the rendezvous
+struct GroupGuard {
+  LocalGroup* g;
+  bool ok = false;
+  ~GroupGuard() {
+    if (!ok && g) g->fail();
+  }
+};
+}  // namespace
+
+__global__ void rank_sum_kernel(const double* __restrict__ stage, int P, size_t count, double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = stage[i];
+    for (int p = 1; p < P; ++p) acc += stage[(size_t)p * count + i];
+    out[i] = acc;
+  }
+}
+
+static void group_allgather(Ctx& c, const double* send, double* recv, size_t count) {
+  LocalGroup& g = *c.group;
+  GroupGuard guard{&g};
+  g.post[c.rank] = send;
+  TTB_CUDA(cudaEventRecord(g.ready[c.rank], c.stream));
+  g.barrier();
+  for (int q = 0; q < g.P; ++q) {
+    if (count == 0) break;
+    if (q != c.rank) TTB_CUDA(cudaStreamWaitEvent(c.stream, g.ready[q], 0));
+    TTB_CUDA(cudaMemcpyAsync(recv + (size_t)q * count, g.post[q], count * sizeof(double), cudaMemcpyDefault, c.stream));
+  }
+  TTB_CUDA(cudaEventRecord(g.done[c.rank], c.stream));
+  g.barrier();
+  for (int q = 0; q < g.P; ++q)
+    if (q != c.rank) TTB_CUDA(cudaStreamWaitEvent(c.stream, g.done[q], 0));
+  guard.ok = true;
+}
 
 // ---- NCCL through dlopen -------------------------------------------------
 struct NcclApi {
@@ -124,6 +224,12 @@ void Ctx::collect(bool all) {
 }
 
 void Ctx::allgather(const double* send, double* recv, size_t count) {
+  if (group) {
+    g_comm[0] += 1;
+    g_comm[1] += (long long)count * (nranks - 1);
+    group_allgather(*this, send, recv, count);
+    return;
+  }
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
   g_comm[0] += 1;
   g_comm[1] += (long long)count * (nranks - 1);
@@ -131,6 +237,20 @@ void Ctx::allgather(const double* send, double* recv, size_t count) {
 }
 
 void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
+  if (group) {
+    TTB_CHECK(send != recv, TTB_ERR_CONTRACT, "allreduce: in-place reduction is not supported");
+    g_comm[2] += 1;
+    g_comm[3] += (long long)count;
+    double* stage = (double*)alloc(std::max<size_t>(1, count * nranks) * sizeof(double));
+    group_allgather(*this, send, stage, count);
+    if (count > 0) {
+      const int grid = (int)std::min<size_t>(1024, (count + 255) / 256);
+      rank_sum_kernel<<<grid, 256, 0, stream>>>(stage, nranks, count, recv);
+      TTB_LAUNCHED();
+    }
+    free(stage);
+    return;
+  }
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
   g_comm[2] += 1;
   g_comm[3] += (long long)count;
@@ -139,6 +259,37 @@ void Ctx::allreduce_sum(const double* send, double* recv, size_t count) {
 
 void Ctx::sendrecv(int npeers, const int* peers, const double* const* send, const int64_t* send_n,
                    double* const* recv, const int64_t* recv_n) {
+  if (group) {
+    // every rank takes part in the rendezvous (its peer list may be empty)
+    LocalGroup& g = *group;
+    GroupGuard guard{&g};
+    const int P = g.P;
+    for (int k = 0; k < npeers; ++k) {
+      TTB_CHECK(peers[k] >= 0 && peers[k] < P && peers[k] != rank, TTB_ERR_CONTRACT, "sendrecv: bad peer");
+      g.p2p[(size_t)rank * P + peers[k]] = {send[k], send_n[k]};
+      g_comm[2] += (send_n[k] > 0) + (recv_n[k] > 0);
+      g_comm[3] += send_n[k];
+    }
+    TTB_CUDA(cudaEventRecord(g.ready[rank], stream));
+    g.barrier();
+    for (int k = 0; k < npeers; ++k) {
+      if (recv_n[k] <= 0) continue;
+      const auto& src = g.p2p[(size_t)peers[k] * P + rank];
+      TTB_CHECK(src.second == recv_n[k] && src.first, TTB_ERR_CONTRACT,
+                "sendrecv: peer " + std::to_string(peers[k]) + " sends " + std::to_string(src.second) +
+                    " values, " + std::to_string(recv_n[k]) + " expected");
+      TTB_CUDA(cudaStreamWaitEvent(stream, g.ready[peers[k]], 0));
+      TTB_CUDA(cudaMemcpyAsync(recv[k], src.first, (size_t)recv_n[k] * sizeof(double), cudaMemcpyDefault, stream));
+    }
+    TTB_CUDA(cudaEventRecord(g.done[rank], stream));
+    g.barrier();
+    for (int k = 0; k < npeers; ++k) {
+      TTB_CUDA(cudaStreamWaitEvent(stream, g.done[peers[k]], 0));
+      g.p2p[(size_t)rank * P + peers[k]] = {nullptr, 0};
+    }
+    guard.ok = true;
+    return;
+  }
   if (npeers == 0) return;
   TTB_CHECK(nccl_comm, TTB_ERR_CONTRACT, "multi-rank call without an initialised communicator");
   TTB_CHECK(g_nccl.send && g_nccl.recv && g_nccl.groupStart && g_nccl.groupEnd, TTB_ERR_NCCL,
@@ -298,6 +449,52 @@ int ttb_ctx_trim(ttb_ctx* ctx) {
   cudaMemPool_t pool;
   TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
   TTB_CUDA(cudaMemPoolTrimTo(pool, 0));
+  TTB_TRY_END
+}
+
+int ttb_group_create(int nranks, ttb_group** out) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(out, TTB_ERR_CONTRACT, "null output pointer");
+  TTB_CHECK(nranks >= 1 && nranks <= 1024, TTB_ERR_CONTRACT, "group size must be in [1, 1024]");
+  *out = reinterpret_cast<ttb_group*>(new LocalGroup(nranks));
+  TTB_TRY_END
+}
+
+int ttb_group_destroy(ttb_group* grp) {
+  TTB_TRY_BEGIN
+  if (grp) {
+    LocalGroup* g = reinterpret_cast<LocalGroup*>(grp);
+    for (auto e : g->ready)
+      if (e) cudaEventDestroy(e);
+    for (auto e : g->done)
+      if (e) cudaEventDestroy(e);
+    delete g;
+  }
+  TTB_TRY_END
+}
+
+int ttb_group_abort(ttb_group* grp) {
+  TTB_TRY_BEGIN
+  if (grp) reinterpret_cast<LocalGroup*>(grp)->fail();
+  TTB_TRY_END
+}
+
+int ttb_ctx_join_group(ttb_ctx* ctx, ttb_group* grp, int rank) {
+  TTB_TRY_BEGIN
+  TTB_CHECK(ctx && grp, TTB_ERR_CONTRACT, "null context or group");
+  LocalGroup* g = reinterpret_cast<LocalGroup*>(grp);
+  TTB_CHECK(rank >= 0 && rank < g->P, TTB_ERR_CONTRACT, "bad rank");
+  TTB_CHECK(!ctx->c.nccl_comm && !ctx->c.group, TTB_ERR_CONTRACT, "context already has a communicator");
+  TTB_CUDA(cudaSetDevice(ctx->c.device));
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    TTB_CHECK(!g->ready[rank], TTB_ERR_CONTRACT, "rank " + std::to_string(rank) + " already joined");
+    TTB_CUDA(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+    TTB_CUDA(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
+  }
+  ctx->c.group = g;
+  ctx->c.nranks = g->P;
+  ctx->c.rank = rank;
   TTB_TRY_END
 }
 

@@ -11,7 +11,8 @@
 
 namespace ttb {
 
-struct NcclApi;  // defined in ctx.cu
+struct NcclApi;     // defined in ctx.cu
+struct LocalGroup;  // defined in ctx.cu: in-process emulated collectives
 extern double g_host_alloc_ms;  // diagnostics: host time in cudaMallocAsync
 
 struct Ctx {
@@ -21,6 +22,11 @@ struct Ctx {
   int nranks = 1;
   int rank = 0;
   void* nccl_comm = nullptr;
+  // in-process group (ttb_group_create / ttb_ctx_join_group): P contexts in
+  // one process, one host thread each, exchanging device buffers by
+  // stream-ordered copies with host rendezvous -- the same call sites as
+  // NCCL, for running the multi-rank path on one device
+  LocalGroup* group = nullptr;
   cudaEvent_t ev = nullptr;
   cudaStream_t side = nullptr;  // second stream for off-critical-path work (lazily created)
 

@@ -113,7 +113,11 @@ static void svd_of_rt(Ctx& ctx, const double* R, int b, double eps, int max_rank
   int hinfo[4] = {0, 0, 0, 0};
   ctx.read_small(o.info, 4 * sizeof(int), hinfo);
   prof_note("svd_sweeps", hinfo[3]);
-  TTB_CHECK(hinfo[2] == 0, TTB_ERR_NUMERIC, "non-finite entries in SVD input");
+  if (hinfo[2] != 0) {
+    ctx.free(o.mem);
+    o.mem = nullptr;
+    TTB_THROW(TTB_ERR_NUMERIC, "non-finite entries in SVD input");
+  }
   o.keep = hinfo[0];
   o.capped = hinfo[1];
 }
@@ -478,6 +482,49 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   int64_t maxcore = 0;
   for (int n = 0; n < N; ++n) maxcore = std::max(maxcore, r[n] * d[n] * r[n + 1]);
   double* scratch = implicit ? nullptr : (double*)ctx.alloc((size_t)std::max<int64_t>(maxcore, 1) * sizeof(double));
+  // unwind (a NumericError from the SVD of non-finite data, a CUDA error):
+  // hand every live workspace block back to the pool, after the side stream
+  // drained into the main stream, so the context stays usable
+  Ctx sctx = ctx;
+  bool side_used = false;
+  Tsqr f2cur;
+  SvdOut socur;
+  struct PendingOut {
+    bool on = false;
+    Tsqr f2;
+    SvdOut so;
+    Panel out;
+    int n = 0;
+    int64_t count = 0;
+  } pend;
+  struct Unwind {
+    Ctx& ctx;
+    Ctx& sctx;
+    bool& side_used;
+    std::vector<Tsqr>& facs;
+    double*& scratch;
+    Tsqr& f2cur;
+    SvdOut& socur;
+    PendingOut& pend;
+    bool armed = true;
+    ~Unwind() {
+      if (!armed) return;
+      try {
+        if (side_used) side_join(ctx, sctx);
+        for (auto& f : facs)
+          if (f.mem) tsqr_release(ctx, f);
+        if (f2cur.mem) tsqr_release(ctx, f2cur);
+        if (socur.mem) ctx.free(socur.mem);
+        if (pend.on) {
+          if (pend.f2.mem) tsqr_release(ctx, pend.f2);
+          if (pend.so.mem) ctx.free(pend.so.mem);
+        }
+        if (scratch) ctx.free(scratch);
+        ctx.collect(true);
+      } catch (...) {
+      }
+    }
+  } unwind{ctx, sctx, side_used, facs, scratch, f2cur, socur, pend};
 
   // ---- orthonormalization sweep (implicit Q kept for *I variants) ----
   const double* last = nullptr;
@@ -529,6 +576,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     }
     for (int n = 0; n <= N; ++n) out_ranks[n] = 1;
     meta[3] = 1.0;
+    unwind.armed = false;
     if (scratch) ctx.free(scratch);
     if (io)
       for (int n = 0; n < N; ++n) io->ready(n, out[n], d[n], ctx.stream);
@@ -544,20 +592,12 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   // main stream sits in the one-CTA SVD instead of competing with the
   // critical carry apply.
   bool violated = false;
-  Ctx sctx = ctx;
   sctx.stream = ctx.side_stream();
   sctx.deferred.clear();  // deferred frees belong to the main context only
-  struct Deferred {
-    bool on = false;
-    Tsqr f2;
-    SvdOut so;
-    Panel out;
-    int n = 0;
-    int64_t count = 0;
-  } pend;
   auto flush = [&]() {
     if (!pend.on) return;
     side_begin(ctx, sctx);  // after everything enqueued on main so far
+    side_used = true;
     tsqr_apply(sctx, pend.f2, pend.so.Vk, pend.so.keep, pend.out);
     if (io) io->ready(pend.n, pend.out.base, pend.count, sctx.stream);
     ctx.free_after(pend.f2.mem, sctx.stream);  // returned to the pool on the main stream
@@ -568,10 +608,10 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   if (left_first) {
     for (int n = N - 1; n >= 1; --n) {
       const int b = (int)r[n];
-      Tsqr f2;
+      Tsqr& f2 = f2cur;
       { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2); }
       { HostTimer ht("flush", &t_flush); flush(); }  // previous step's output core overlaps this step's SVD
-      SvdOut so;
+      SvdOut& so = socur;
       { HostTimer ht("svd", &t_svd); svd_of_rt(ctx, f2.R, b, eps, mr, so); }
       const int keep = so.keep;
       violated |= so.capped != 0;
@@ -587,6 +627,8 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
       pend.on = true;
       pend.f2 = f2;
       pend.so = so;
+      f2cur = Tsqr();
+      socur = SvdOut();
       pend.out = panel_of(out[n], keep, d[n], r[n + 1], 1);
       pend.n = n;
       pend.count = (int64_t)keep * d[n] * r[n + 1];
@@ -597,10 +639,10 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   } else {
     for (int n = 0; n < N - 1; ++n) {
       const int b = (int)r[n + 1];
-      Tsqr f2;
+      Tsqr& f2 = f2cur;
       tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 0), f2);
       flush();
-      SvdOut so;
+      SvdOut& so = socur;
       svd_of_rt(ctx, f2.R, b, eps, mr, so);
       const int keep = so.keep;
       violated |= so.capped != 0;
@@ -615,6 +657,8 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
       pend.on = true;
       pend.f2 = f2;
       pend.so = so;
+      f2cur = Tsqr();
+      socur = SvdOut();
       pend.out = panel_of(out[n], r[n], d[n], keep, 0);
       pend.n = n;
       pend.count = r[n] * d[n] * (int64_t)keep;
@@ -624,6 +668,7 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     if (io) io->ready(N - 1, out[N - 1], r[N - 1] * d[N - 1] * r[N], ctx.stream);
   }
   side_join(ctx, sctx);
+  unwind.armed = false;
   ctx.collect(true);
   if (scratch) ctx.free(scratch);
   meta[2] = violated ? 1.0 : 0.0;

@@ -255,11 +255,7 @@ static bool fold_tma(Ctx& ctx, const SkinnyArgs& a) {
   const int ldS = ((a.K + 11) & ~15) + 4, MP = (a.M + 15) & ~15;
   const size_t bst = RIGHT ? (size_t)a.K * (kFoldJ + 4) : (size_t)a.K * kFoldJ;
   const size_t smem = (16 + (size_t)MP * ldS + 16 + (size_t)kFoldStages * bst) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(fold_kernel<RIGHT, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  smem_attr((const void*)fold_kernel<RIGHT, J>, 227 * 1024);
   if (smem * kFoldMinB > 227 * 1024) return false;
   const int64_t nch = (a.N + kFoldJ - 1) / kFoldJ;
   const int grid = (int)std::min<int64_t>(nch, (int64_t)kFoldMinB * ctx.num_sms);

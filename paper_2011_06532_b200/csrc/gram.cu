@@ -773,11 +773,7 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
     per_cta = (per_cta + kG16NS - 1) / kG16NS * kG16NS;
     grid = (int)((I + per_cta - 1) / per_cta);
     double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
-    static bool attr = false;
-    if (!attr) {
-      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    smem_attr((const void*)gram16_kernel<false>, smem);
     ProfScope ps("gram", ctx.stream);
     gram16_kernel<false><<<grid, kG16NT, smem, ctx.stream>>>(W, X, Y, nullptr, I, per_cta, part, ticket, Wn,
                                                              nullptr);
@@ -845,7 +841,7 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
     g.part = part;
     ProfScope ps("gram", ctx.stream);
     auto launch = [&](auto kern, int nt) {
-      TTB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_attr((const void*)kern, smem);
       kern<<<grid, nt, smem, ctx.stream>>>(g);
     };
     if (rbr <= 16) launch(gram2_kernel<2, 512>, 512);
@@ -873,7 +869,7 @@ void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t 
   grid = (int)((I + per_cta - 1) / per_cta);
   double* part = (double*)ctx.alloc((size_t)grid * cnt * sizeof(double));
   GramArgs a{W, X, Y, (int)ral, (int)rar, (int)rbl, (int)rbr, I, ns, per_cta, part};
-  TTB_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_attr((const void*)gram_kernel, smem);
   ProfScope ps("gram", ctx.stream);
   gram_kernel<<<grid, kGrNT, smem, ctx.stream>>>(a);
   TTB_LAUNCHED();
@@ -912,11 +908,7 @@ void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* 
     per_cta = (per_cta + ns - 1) / ns * ns;
     grid = (int)((I + per_cta - 1) / per_cta);
     double* part = (double*)ctx.alloc((size_t)grid * 256 * sizeof(double));
-    static bool attr = false;
-    if (!attr) {
-      TTB_CUDA(cudaFuncSetAttribute(gram16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    smem_attr((const void*)gram16_kernel<true>, smem);
     ProfScope ps("gram", ctx.stream);
     gram16_kernel<true><<<grid, kG16sNT, smem, ctx.stream>>>(PL, X, nullptr, perm, I, per_cta, part, ticket, Wrec,
                                                             ctx.flag());

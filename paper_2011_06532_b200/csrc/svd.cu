@@ -340,11 +340,7 @@ __global__ void svd_u_kernel(const double* C, const double* s, int m, int keep, 
 void jacobi_svd(Ctx& ctx, const double* A, int lda, int m, int n, bool transA, double eps, int max_rank,
                 double* C, double* Vk, double* s, int* info, double* dinfo) {
   TTB_CHECK(m >= n && n >= 1 && m <= kSvdMax, TTB_ERR_CAPABILITY, "Jacobi SVD: need 1 <= n <= m <= 64");
-  static bool attr = false;
-  if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SvdSmem)));
-    attr = true;
-  }
+  smem_attr((const void*)jacobi_svd_kernel, sizeof(SvdSmem));
   ProfScope ps("jacobi_svd", ctx.stream);
   static_assert(kSvdMax / 2 <= kHalf / kGrp, "one pair slot per thread group");
   jacobi_svd_kernel<<<1, kSvdNT, sizeof(SvdSmem), ctx.stream>>>(A, lda, m, n, transA ? 1 : 0, eps, max_rank, C, Vk,

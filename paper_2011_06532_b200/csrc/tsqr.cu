@@ -40,6 +40,10 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
 
   double A[C::RPL][C::CPL];
   init_ring<C>(sm);
+  if (ntiles == 0) {  // no rows (an idle rank): R = 0
+    for (int idx = threadIdx.x; idx < C::BMAX * C::BMAX; idx += C::NT) sm.Rs[idx] = 0.0;
+    __syncthreads();
+  }
   for (int t = 0; t < ntiles; ++t) {
     const int64_t ia = s0 + (int64_t)t * ni;
     const int nsl = (int)min64(ni, n_g - (int64_t)t * ni);
@@ -649,11 +653,7 @@ size_t tree_smem() {
 
 template <class C>
 void set_smem_attr(const void* fn) {
-  static std::vector<const void*> done;  // per kernel (configs may coincide)
-  for (const void* f : done)
-    if (f == fn) return;
-  TTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<C>)));
-  done.push_back(fn);
+  smem_attr(fn, sizeof(TileSmem<C>));
 }
 
 template <class LC_, class TC_>
@@ -667,15 +667,7 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   TTB_LAUNCHED();
   }
   auto tree = tsqr_tree_kernel<TC_>;
-  {
-    static std::vector<const void*> done;
-    bool seen = false;
-    for (const void* p : done) seen |= (p == (const void*)tree);
-    if (!seen) {
-      TTB_CUDA(cudaFuncSetAttribute((const void*)tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem<TC_>()));
-      done.push_back((const void*)tree);
-    }
-  }
+  smem_attr((const void*)tree, tree_smem<TC_>());
   // levels [0, n) of a tree over n_in complete inputs, one launch
   auto run_tree = [&](const double* rin, int n_in, int nlev, double* const* Ys, double* const* Ts,
                       double* const* Rs) {
@@ -845,13 +837,9 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   double* lev[2] = {scr, scr + maxlev * bk};
   double* ubuf = scr + 2 * maxlev * bk;
   double* z0buf = ubuf + ntiles * b * ldpad(k);
-  static bool attr = false;
-  if (!attr) {
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_tree_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  smem_attr((const void*)tsqr_tree_apply_kernel, 227 * 1024);
+  smem_attr((const void*)tsqr_chain_kernel, 227 * 1024);
+  smem_attr((const void*)tsqr_product_kernel, 227 * 1024);
   const double* cur = z;
   const double* Dp = f.D;
   int which = 0;

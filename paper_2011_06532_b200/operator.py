@@ -158,7 +158,7 @@ def _halo(comm, slab, plan, send_idx):
     rl, dloc, rr = slab.shape
     per = rl * rr
     halo = torch.empty(max(plan.nhalo * per, 1), dtype=torch.float64, device=comm.device)
-    if comm.size == 1 or (not plan.send and not plan.recv):
+    if comm.size == 1 or (not plan.send and not plan.recv and not comm.rendezvous):
         return halo
     lib = _lib.load()
     ctx = comm.ctx()
