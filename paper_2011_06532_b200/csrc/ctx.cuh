@@ -90,6 +90,8 @@ struct Tsqr {
 };
 
 int tsqr_class(int b);
+// blocked (panel warp + fp64 MMA) leaf for 32 < b <= 64 (leaf2.cu)
+void launch_leaf2(Ctx& ctx, const Panel& panel, const LeafPlan& plan, double* Y, double* T, double* Rleaf);
 void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f);
 // out (view with k columns, same slicing as the factored panel) = Q [D z; 0]
 void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& out);

@@ -662,9 +662,14 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   auto leaf = tsqr_leaf_kernel<LC_>;
   set_smem_attr<LC_>((const void*)leaf);
   {
-  ProfScope ps("tsqr_leaf", st);
-  leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
-  TTB_LAUNCHED();
+    static const bool v1 = getenv("TTB_LEAF_V1") != nullptr;  // A/B switch: the unblocked column pipeline
+    ProfScope ps("tsqr_leaf", st);
+    if (f.cls == 64 && !v1) {
+      launch_leaf2(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
+    } else {
+      leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
+      TTB_LAUNCHED();
+    }
   }
   auto tree = tsqr_tree_kernel<TC_>;
   smem_attr((const void*)tree, tree_smem<TC_>());
