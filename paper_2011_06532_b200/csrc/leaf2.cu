@@ -22,7 +22,7 @@
 //    the trailing ones for the update, the finished ones for V^T V) and one
 //    reflector-scalar chain.  It also forms the panel's 8 x 8 T by the
 //    dlarft recurrence and writes Y_p (256 x 8) to shared memory.
-//  * eight COMPUTE WARPS hold the tile (32 rows x 64 columns each) in
+//  * seven COMPUTE WARPS hold the tile (40 or 32 rows x 64 columns each) in
 //    registers, TRANSPOSED, in the D-fragment layout of the fp64 MMA
 //    m16n8k8 (m = column, n = row).  A D fragment of that product is, with
 //    the contraction index permuted inside each 8-block (k = t <-> row 2t,
@@ -51,13 +51,38 @@ namespace ttb {
 
 namespace lf2 {
 
-constexpr int NCW = 8;               // compute warps
+#ifdef TTB_LF2_CLK
+// debug: cycle stamps of CTA 0's first 64 panels, 8 per panel
+__device__ long long g_lf2clk[64 * 8];
+__device__ long long g_lf2col[64 * 12];  // panel warp: load done, after each column, after writes
+#define LF2_COL(gp, slot)                                                              \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gp) < 64) g_lf2col[(gp) * 12 + (slot)] = clock64(); \
+  } while (0)
+#define LF2_CLK(gp, slot)                                                               \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gp) < 64) g_lf2clk[(gp) * 8 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define LF2_CLK(gp, slot) \
+  do {                    \
+  } while (0)
+#define LF2_COL(gp, slot) \
+  do {                    \
+  } while (0)
+#endif
+
+// 8 warps in all, two per SM sub-partition, so every warp may use up to 255
+// registers: seven compute warps share the 256 tile rows (warps 0-3 hold 40
+// rows = 5 n8 tiles, warps 4-6 hold 32) and one panel warp
+constexpr int NCW = 7;               // compute warps
 constexpr int NTC = NCW * 32;        // compute threads
 constexpr int NT = NTC + 32;         // + the panel warp
 constexpr int MC = 256;              // tile rows
 constexpr int BM = 64;               // max columns
 constexpr int NMT = 4;               // m16 column tiles
-constexpr int NNT = 4;               // n8 row tiles per compute warp (32 rows)
+constexpr int NNT_MAX = 5;           // n8 row tiles per compute warp (40 or 32 rows)
+__device__ __forceinline__ int warp_rbase(int w) { return w < 4 ? 40 * w : 160 + 32 * (w - 4); }
 constexpr int NB = 8;                // panel width
 constexpr int WNLD = 12;             // row stride of Wneg (conflict-free A fragments)
 
@@ -96,7 +121,8 @@ __device__ __forceinline__ void mma1688(double (&d)[4], double a0, double a1, do
 // ------------------------------------------------------------------------
 // panel warp: QR of [P (8 x 8); A (256 x 8)] with pivots in P
 // ------------------------------------------------------------------------
-__device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, int c0, int nbp, int b, bool head) {
+__device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, int c0, int nbp, int b, bool head,
+                                             unsigned gp) {
   const int lane = threadIdx.x & 31;
   double a[8][8], pr[8], tr[8];
   // A part: head tiles exclude rows < c0 + 8 (R above, the pivot block itself)
@@ -116,9 +142,12 @@ __device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, 
     tr[c] = 0.0;
   }
   const bool plane = lane < NB;
+  LF2_COL(gp, 0);
+  // every lane runs all 8 column steps (no data-dependent exit around the
+  // shuffles); columns past the panel width are zero and get tau = 0
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    if (j >= nbp) break;
+    const bool act = j < nbp;
     const bool below = plane && lane > j;  // pivot-block rows below the pivot
     // partial sums: acc[j] = |x|^2 below the pivot, acc[k] = x . col k (raw x)
     double acc[8];
@@ -145,6 +174,11 @@ __device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, 
     for (int k = 0; k < 8; ++k) prj[k] = __shfl_sync(0xffffffffu, pr[k], j);
     double beta, tau, scal, bv;
     reflector_scalars<false>(prj[j], acc[j], beta, tau, scal, bv);
+    if (!act) {
+      tau = 0.0;
+      scal = 0.0;
+      beta = prj[j];
+    }
     // d_k = v . a_k (k > j) and G[k][j] = v_k . v_j (k < j): the same formula
     double dd[8];
 #pragma unroll
@@ -168,6 +202,7 @@ __device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, 
 #pragma unroll
     for (int m = 0; m < j; ++m) sum = fma(tr[m], dd[m], sum);
     tr[j] = lane < j ? -tau * sum : (lane == j ? tau : 0.0);
+    LF2_COL(gp, 1 + j);
   }
   // Y_p -> B (head: rows < c0 zero, pivot rows unit lower from the block)
 #pragma unroll
@@ -185,6 +220,7 @@ __device__ __forceinline__ void panel_factor(Smem& sm, double* Bp, double* Tpp, 
       Tpp[lane * NB + c] = tr[c];
     }
   }
+  LF2_COL(gp, 9);
 }
 
 // ------------------------------------------------------------------------
@@ -197,38 +233,47 @@ struct TileIO {
   int nsl;
 };
 
-__device__ __forceinline__ double tile_at(const TileIO& io, int r, int k, int b) {
-  if (r >= io.nsl * io.rs || k >= b) return 0.0;
-  int si, w;
-  tile_row(io.P.trans, r, io.nsl, io.rs, si, w);
-  return __ldg(&io.P.base[io.P.addr(w, io.ia + si, k)]);
-}
 
 // registers: A[mt][nt][z], z = {(col g, row 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)} of the
 // m16 column tile mt and the warp's n8 row tile nt
-__device__ __forceinline__ void load_tile(double (&A)[NMT][NNT][4], const TileIO& io, int b) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+template <int NN>
+__device__ __forceinline__ void load_tile(double (&A)[NMT][NN][4], const TileIO& io, int b, int rbase) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int rows = io.nsl * io.rs;
+  const int64_t cstride = io.P.trans ? 1 : io.P.rl * io.P.I;  // column step of the view
+  const double* base = io.P.base;
 #pragma unroll
-  for (int mt = 0; mt < NMT; ++mt)
+  for (int nt = 0; nt < NN; ++nt) {
+    int64_t off[2];
+    bool ok[2];
 #pragma unroll
-    for (int nt = 0; nt < NNT; ++nt) {
-      const int r = w * 32 + nt * 8 + 2 * t4, c = mt * 16 + g;
-      A[mt][nt][0] = tile_at(io, r, c, b);
-      A[mt][nt][1] = tile_at(io, r + 1, c, b);
-      A[mt][nt][2] = tile_at(io, r, c + 8, b);
-      A[mt][nt][3] = tile_at(io, r + 1, c + 8, b);
+    for (int h = 0; h < 2; ++h) {  // one division pair per row, not per element
+      const int r = rbase + nt * 8 + 2 * t4 + h;
+      int si, w;
+      tile_row(io.P.trans, r, io.nsl, io.rs, si, w);
+      ok[h] = r < rows;
+      off[h] = ok[h] ? io.P.addr(w, io.ia + si, 0) : 0;
     }
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) {
+      const int c = mt * 16 + g;
+      A[mt][nt][0] = ok[0] && c < b ? __ldg(base + off[0] + cstride * c) : 0.0;
+      A[mt][nt][1] = ok[1] && c < b ? __ldg(base + off[1] + cstride * c) : 0.0;
+      A[mt][nt][2] = ok[0] && c + 8 < b ? __ldg(base + off[0] + cstride * (c + 8)) : 0.0;
+      A[mt][nt][3] = ok[1] && c + 8 < b ? __ldg(base + off[1] + cstride * (c + 8)) : 0.0;
+    }
+  }
 }
 
 // panel p's columns of the register tile -> B (all 256 rows); head tiles also
 // publish the finished R entries above the panel's pivot block
-template <int MT>
-__device__ __forceinline__ void handoff_mt(const double (&A)[NMT][NNT][4], int h, double* Bn, Smem& sm, bool head,
-                                           int c0) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+template <int MT, int NN>
+__device__ __forceinline__ void handoff_mt(const double (&A)[NMT][NN][4], int h, double* Bn, Smem& sm, bool head,
+                                           int c0, int rbase) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int nt = 0; nt < NNT; ++nt) {
-    const int r = w * 32 + nt * 8 + 2 * t4;
+  for (int nt = 0; nt < NN; ++nt) {
+    const int r = rbase + nt * 8 + 2 * t4;
     const double v0 = h ? A[MT][nt][2] : A[MT][nt][0];
     const double v1 = h ? A[MT][nt][3] : A[MT][nt][1];
     Bn[bsw(r, g)] = v0;
@@ -240,23 +285,25 @@ __device__ __forceinline__ void handoff_mt(const double (&A)[NMT][NNT][4], int h
   }
 }
 
-__device__ __forceinline__ void handoff(const double (&A)[NMT][NNT][4], int p, double* Bn, Smem& sm, bool head) {
+template <int NN>
+__device__ __forceinline__ void handoff(const double (&A)[NMT][NN][4], int p, double* Bn, Smem& sm, bool head,
+                                        int rbase) {
   const int c0 = p * NB, h = p & 1;
   switch (p >> 1) {
-    case 0: handoff_mt<0>(A, h, Bn, sm, head, c0); break;
-    case 1: handoff_mt<1>(A, h, Bn, sm, head, c0); break;
-    case 2: handoff_mt<2>(A, h, Bn, sm, head, c0); break;
-    default: handoff_mt<3>(A, h, Bn, sm, head, c0); break;
+    case 0: handoff_mt<0, NN>(A, h, Bn, sm, head, c0, rbase); break;
+    case 1: handoff_mt<1, NN>(A, h, Bn, sm, head, c0, rbase); break;
+    case 2: handoff_mt<2, NN>(A, h, Bn, sm, head, c0, rbase); break;
+    default: handoff_mt<3, NN>(A, h, Bn, sm, head, c0, rbase); break;
   }
 }
 
 // the factored panel (V form) back into the register tile
-template <int MT>
-__device__ __forceinline__ void reload_mt(double (&A)[NMT][NNT][4], int h, const double* Yb) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+template <int MT, int NN>
+__device__ __forceinline__ void reload_mt(double (&A)[NMT][NN][4], int h, const double* Yb, int rbase) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int nt = 0; nt < NNT; ++nt) {
-    const int r = w * 32 + nt * 8 + 2 * t4;
+  for (int nt = 0; nt < NN; ++nt) {
+    const int r = rbase + nt * 8 + 2 * t4;
     const double v0 = Yb[bsw(r, g)], v1 = Yb[bsw(r + 1, g)];
     if (h) {
       A[MT][nt][2] = v0;
@@ -268,23 +315,24 @@ __device__ __forceinline__ void reload_mt(double (&A)[NMT][NNT][4], int h, const
   }
 }
 
-__device__ __forceinline__ void reload(double (&A)[NMT][NNT][4], int p, const double* Yb) {
+template <int NN>
+__device__ __forceinline__ void reload(double (&A)[NMT][NN][4], int p, const double* Yb, int rbase) {
   const int h = p & 1;
   switch (p >> 1) {
-    case 0: reload_mt<0>(A, h, Yb); break;
-    case 1: reload_mt<1>(A, h, Yb); break;
-    case 2: reload_mt<2>(A, h, Yb); break;
-    default: reload_mt<3>(A, h, Yb); break;
+    case 0: reload_mt<0, NN>(A, h, Yb, rbase); break;
+    case 1: reload_mt<1, NN>(A, h, Yb, rbase); break;
+    case 2: reload_mt<2, NN>(A, h, Yb, rbase); break;
+    default: reload_mt<3, NN>(A, h, Yb, rbase); break;
   }
 }
 
 // W^T partial of m-tile MT over this warp's rows -> sm.Wpart[warp]
-template <int MT>
-__device__ __forceinline__ void wpart_mt(const double (&A)[NMT][NNT][4], const double (&yw)[NNT][2], Smem& sm) {
+template <int MT, int NN>
+__device__ __forceinline__ void wpart_mt(const double (&A)[NMT][NN][4], const double (&yw)[NN][2], Smem& sm) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int nt = 0; nt < NNT; ++nt)
+  for (int nt = 0; nt < NN; ++nt)
     mma1688(acc, A[MT][nt][0], A[MT][nt][2], A[MT][nt][1], A[MT][nt][3], yw[nt][0], yw[nt][1]);
   double* wp = sm.Wpart[w];
   *reinterpret_cast<double2*>(&wp[(MT * 16 + g) * NB + 2 * t4]) = make_double2(acc[0], acc[1]);
@@ -292,14 +340,14 @@ __device__ __forceinline__ void wpart_mt(const double (&A)[NMT][NNT][4], const d
 }
 
 // A^T[m-tile MT] += Wneg^T-fragment x Y_p^T
-template <int MT>
-__device__ __forceinline__ void update_mt(double (&A)[NMT][NNT][4], const double (&yu)[NNT][2], const Smem& sm) {
+template <int MT, int NN>
+__device__ __forceinline__ void update_mt(double (&A)[NMT][NN][4], const double (&yu)[NN][2], const Smem& sm) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
   const double* wn = sm.Wneg;
   const double a0 = wn[(MT * 16 + g) * WNLD + t4], a1 = wn[(MT * 16 + g + 8) * WNLD + t4];
   const double a2 = wn[(MT * 16 + g) * WNLD + t4 + 4], a3 = wn[(MT * 16 + g + 8) * WNLD + t4 + 4];
 #pragma unroll
-  for (int nt = 0; nt < NNT; ++nt) mma1688(A[MT][nt], a0, a1, a2, a3, yu[nt][0], yu[nt][1]);
+  for (int nt = 0; nt < NN; ++nt) mma1688(A[MT][nt], a0, a1, a2, a3, yu[nt][0], yu[nt][1]);
 }
 
 // dispatch a per-m-tile routine over a mask of m-tiles
@@ -336,7 +384,152 @@ __device__ __forceinline__ double reduce_col(const Smem& sm, const double* Tp, i
 
 using namespace lf2;
 
-__global__ void __maxnreg__(224)
+template <int NN>
+__device__ __forceinline__ void compute_role(Smem& sm, const Panel& P, const LeafPlan& plan, double* __restrict__ Yg,
+                                             double* __restrict__ Tg, int rbase) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gcta = blockIdx.x;
+  const int b = plan.b, rs = plan.rs, ni = plan.ni;
+  const int np = (b + NB - 1) / NB;
+  const int64_t n_g = plan.count(gcta), s0 = plan.start(gcta);
+  const int ntiles = plan.tiles_of(n_g);
+  const int64_t tb = plan.tile_base(gcta);
+    const int g = lane >> 2, t4 = lane & 3;
+    double A[NMT][NN][4];
+    unsigned gp = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const bool head = t == 0;
+      TileIO io;
+      io.P = P;
+      io.rs = rs;
+      io.ia = s0 + (int64_t)t * ni;
+      io.nsl = (int)min64(ni, n_g - (int64_t)t * ni);
+      load_tile<NN>(A, io, b, rbase);
+      handoff<NN>(A, 0, sm.B[gp & 1], sm, head, rbase);
+      csync();
+      if (tid == 0) mbar_arrive(&sm.ready);
+      for (int p = 0; p < np; ++p, ++gp) {
+        const int c0 = p * NB;
+        const bool has_next = p + 1 < np;
+        const int mt1 = has_next ? (p + 1) >> 1 : -1;
+        if (threadIdx.x == 0) LF2_CLK(gp, 3);
+        mbar_wait(&sm.done, gp & 1);
+        if (threadIdx.x == 0) LF2_CLK(gp, 4);
+        const double* Yb = sm.B[gp & 1];
+        const double* Tp = sm.Tpp[gp & 1];
+        reload<NN>(A, p, Yb, rbase);
+        double yw[NN][2], yu[NN][2];
+#pragma unroll
+        for (int nt = 0; nt < NN; ++nt) {
+          const int r = rbase + nt * 8;
+          yw[nt][0] = Yb[bsw(r + 2 * t4, g)];
+          yw[nt][1] = Yb[bsw(r + 2 * t4 + 1, g)];
+          yu[nt][0] = Yb[bsw(r + g, t4)];
+          yu[nt][1] = Yb[bsw(r + g, t4 + 4)];
+        }
+        // ---- critical path: the next panel's columns ----
+        if (has_next) {
+#define LF2_W(MT) wpart_mt<MT, NN>(A, yw, sm)
+          LF2_FOR_MT(1 << mt1, LF2_W);
+          csync();
+          {  // 128 (column, reflector) items; threads >= 128 recompute 0..95 and store nothing
+            const int item = tid & 127;
+            const int k = mt1 * 16 + (item >> 3), j = item & 7;
+            double raw;
+            const double wv = reduce_col(sm, Tp, k, j, c0, head, raw);
+            const bool upd = k >= c0 + NB && k < b;  // panel p+1 (and p+2 when they share the m-tile)
+            if (tid < 128) {
+              sm.Wneg[k * WNLD + j] = upd ? -wv : 0.0;
+              if (!head && upd) sm.Rs[(c0 + j) + BM * k] -= wv;
+            }
+          }
+          csync();
+#define LF2_U(MT) update_mt<MT, NN>(A, yu, sm)
+          LF2_FOR_MT(1 << mt1, LF2_U);
+          handoff<NN>(A, p + 1, sm.B[(gp + 1) & 1], sm, head, rbase);
+          csync();
+          if (tid == 0) LF2_CLK(gp, 5);
+          if (tid == 0) mbar_arrive(&sm.ready);
+        }
+        // ---- the rest: trailing columns, cross Gram ----
+        const unsigned all = (1u << NMT) - 1;
+        const unsigned rest = has_next ? (all & ~(1u << mt1)) : all;
+#ifndef LF2_DBG_NOREST
+        LF2_FOR_MT(rest, LF2_W);
+#endif
+        csync();
+#pragma unroll
+        for (int rnd = 0; rnd < (BM * NB + NTC - 1) / NTC; ++rnd) {  // uniform trip count (shuffles inside)
+          const int it0 = tid + rnd * NTC;
+          const int it = it0 & (BM * NB - 1);
+          const int k = it >> 3, j = it & 7;
+          double raw;
+          const double wv = reduce_col(sm, Tp, k, j, c0, head, raw);
+          if (it0 < BM * NB && !(has_next && (k >> 4) == mt1)) {
+            const bool upd = k >= c0 + NB && k < b;
+            if (k < c0) sm.Xc[k * NB + j] = raw;
+            sm.Wneg[k * WNLD + j] = upd ? -wv : 0.0;
+            if (!head && upd) sm.Rs[(c0 + j) + BM * k] -= wv;
+          }
+        }
+        csync();
+        // m-tiles holding trailing columns (>= c0 + 8), except the critical one
+        const int first_tr = (c0 + NB) >> 4;
+        unsigned trail = 0;
+        for (int mt = first_tr; mt < NMT; ++mt)
+          if (mt * 16 < b) trail |= 1u << mt;
+        trail &= rest;
+#ifndef LF2_DBG_NOREST
+        LF2_FOR_MT(trail, LF2_U);
+#endif
+#undef LF2_W
+#undef LF2_U
+        // ---- T: diagonal block, then T[0:c0, p] = -T[0:c0, 0:c0] (Xc T_pp) ----
+#ifndef LF2_DBG_NOT
+        for (int it = tid; it < NB * NB; it += NTC) {
+          const int i = it >> 3, j = it & 7;
+          sm.Ts[(c0 + i) + BM * (c0 + j)] = Tp[i * NB + j];
+        }
+        for (int it = tid; it < c0 * NB; it += NTC) {
+          const int k = it >> 3, j = it & 7;
+          double x = 0.0;
+#pragma unroll
+          for (int i = 0; i < NB; ++i) x = fma(sm.Xc[k * NB + i], Tp[i * NB + j], x);
+          sm.Xs[k * NB + j] = x;
+        }
+        csync();
+        for (int it = tid; it < c0 * NB; it += NTC) {
+          const int m = it >> 3, j = it & 7;
+          double x = 0.0;
+          for (int k = m; k < c0; ++k) x = fma(sm.Ts[m + BM * k], sm.Xs[k * NB + j], x);
+          sm.Ts[m + BM * (c0 + j)] = -x;
+        }
+#endif
+        if (tid == 0) LF2_CLK(gp, 6);
+      }
+      csync();
+      // ---- tile outputs: Y (unit-major), T ----
+      const int64_t tile = tb + t;
+      double* Yt = Yg + tile * y_tile_stride(MC, b);
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NN; ++nt) {
+          const int r = rbase + nt * 8 + 2 * t4;
+          const int c = mt * 16 + g;
+          if (c < b) *reinterpret_cast<double2*>(&Yt[y_index(r, c, b)]) = make_double2(A[mt][nt][0], A[mt][nt][1]);
+          if (c + 8 < b)
+            *reinterpret_cast<double2*>(&Yt[y_index(r, c + 8, b)]) = make_double2(A[mt][nt][2], A[mt][nt][3]);
+        }
+      double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
+      for (int idx = tid; idx < b * b; idx += NTC) {
+        const int k = idx % b, j = idx / b;
+        Tt[idx] = k <= j ? sm.Ts[k + BM * j] : 0.0;
+      }
+    }
+}
+
+__global__ void __launch_bounds__(lf2::NT, 1)
 tsqr_leaf2_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __restrict__ Tg,
                   double* __restrict__ Rleaf) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -363,131 +556,19 @@ tsqr_leaf2_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __res
       const bool head = t == 0;
       for (int p = 0; p < np; ++p, ++gp) {
         const int c0 = p * NB, nbp = min(NB, b - c0);
+        LF2_CLK(gp, 0);
         mbar_wait(&sm.ready, gp & 1);
-        panel_factor(sm, sm.B[gp & 1], sm.Tpp[gp & 1], c0, nbp, b, head);
+        LF2_CLK(gp, 1);
+        panel_factor(sm, sm.B[gp & 1], sm.Tpp[gp & 1], c0, nbp, b, head, gp);
         __syncwarp();
+        LF2_CLK(gp, 2);
         if (lane == 0) mbar_arrive(&sm.done);
       }
     }
+  } else if (warp < 4) {
+    compute_role<5>(sm, P, plan, Yg, Tg, warp_rbase(warp));
   } else {
-    // ---------------- compute warps ----------------
-    const int g = lane >> 2, t4 = lane & 3;
-    const int rbase = warp * 32;
-    double A[NMT][NNT][4];
-    unsigned gp = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const bool head = t == 0;
-      TileIO io;
-      io.P = P;
-      io.rs = rs;
-      io.ia = s0 + (int64_t)t * ni;
-      io.nsl = (int)min64(ni, n_g - (int64_t)t * ni);
-      load_tile(A, io, b);
-      handoff(A, 0, sm.B[gp & 1], sm, head);
-      csync();
-      if (tid == 0) mbar_arrive(&sm.ready);
-      for (int p = 0; p < np; ++p, ++gp) {
-        const int c0 = p * NB;
-        const bool has_next = p + 1 < np;
-        const int mt1 = has_next ? (p + 1) >> 1 : -1;
-        mbar_wait(&sm.done, gp & 1);
-        const double* Yb = sm.B[gp & 1];
-        const double* Tp = sm.Tpp[gp & 1];
-        reload(A, p, Yb);
-        double yw[NNT][2], yu[NNT][2];
-#pragma unroll
-        for (int nt = 0; nt < NNT; ++nt) {
-          const int r = rbase + nt * 8;
-          yw[nt][0] = Yb[bsw(r + 2 * t4, g)];
-          yw[nt][1] = Yb[bsw(r + 2 * t4 + 1, g)];
-          yu[nt][0] = Yb[bsw(r + g, t4)];
-          yu[nt][1] = Yb[bsw(r + g, t4 + 4)];
-        }
-        // ---- critical path: the next panel's columns ----
-        if (has_next) {
-#define LF2_W(MT) wpart_mt<MT>(A, yw, sm)
-          LF2_FOR_MT(1 << mt1, LF2_W);
-          csync();
-          if (tid < 128) {
-            const int k = mt1 * 16 + (tid >> 3), j = tid & 7;
-            double raw;
-            const double wv = reduce_col(sm, Tp, k, j, c0, head, raw);
-            const bool upd = k >= c0 + NB && k < b;  // panel p+1 (and p+2 when they share the m-tile)
-            sm.Wneg[k * WNLD + j] = upd ? -wv : 0.0;
-            if (!head && upd) sm.Rs[(c0 + j) + BM * k] -= wv;
-          }
-          csync();
-#define LF2_U(MT) update_mt<MT>(A, yu, sm)
-          LF2_FOR_MT(1 << mt1, LF2_U);
-          handoff(A, p + 1, sm.B[(gp + 1) & 1], sm, head);
-          csync();
-          if (tid == 0) mbar_arrive(&sm.ready);
-        }
-        // ---- the rest: trailing columns, cross Gram ----
-        const unsigned all = (1u << NMT) - 1;
-        const unsigned rest = has_next ? (all & ~(1u << mt1)) : all;
-        LF2_FOR_MT(rest, LF2_W);
-        csync();
-        for (int it = tid; it < BM * NB; it += NTC) {
-          const int k = it >> 3, j = it & 7;
-          if (has_next && (k >> 4) == mt1) continue;  // warp-uniform (16 columns = 4 warps... per 8-lane group)
-          double raw;
-          const double wv = reduce_col(sm, Tp, k, j, c0, head, raw);
-          const bool upd = k >= c0 + NB && k < b;
-          if (k < c0) sm.Xc[k * NB + j] = raw;
-          sm.Wneg[k * WNLD + j] = upd ? -wv : 0.0;
-          if (!head && upd) sm.Rs[(c0 + j) + BM * k] -= wv;
-        }
-        csync();
-        // m-tiles holding trailing columns (>= c0 + 8), except the critical one
-        const int first_tr = (c0 + NB) >> 4;
-        unsigned trail = 0;
-        for (int mt = first_tr; mt < NMT; ++mt)
-          if (mt * 16 < b) trail |= 1u << mt;
-        trail &= rest;
-        LF2_FOR_MT(trail, LF2_U);
-#undef LF2_W
-#undef LF2_U
-        // ---- T: diagonal block, then T[0:c0, p] = -T[0:c0, 0:c0] (Xc T_pp) ----
-        for (int it = tid; it < NB * NB; it += NTC) {
-          const int i = it >> 3, j = it & 7;
-          sm.Ts[(c0 + i) + BM * (c0 + j)] = Tp[i * NB + j];
-        }
-        for (int it = tid; it < c0 * NB; it += NTC) {
-          const int k = it >> 3, j = it & 7;
-          double x = 0.0;
-#pragma unroll
-          for (int i = 0; i < NB; ++i) x = fma(sm.Xc[k * NB + i], Tp[i * NB + j], x);
-          sm.Xs[k * NB + j] = x;
-        }
-        csync();
-        for (int it = tid; it < c0 * NB; it += NTC) {
-          const int m = it >> 3, j = it & 7;
-          double x = 0.0;
-          for (int k = m; k < c0; ++k) x = fma(sm.Ts[m + BM * k], sm.Xs[k * NB + j], x);
-          sm.Ts[m + BM * (c0 + j)] = -x;
-        }
-      }
-      csync();
-      // ---- tile outputs: Y (unit-major), T ----
-      const int64_t tile = tb + t;
-      double* Yt = Yg + tile * y_tile_stride(MC, b);
-#pragma unroll
-      for (int mt = 0; mt < NMT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NNT; ++nt) {
-          const int r = rbase + nt * 8 + 2 * t4;
-          const int c = mt * 16 + g;
-          if (c < b) *reinterpret_cast<double2*>(&Yt[y_index(r, c, b)]) = make_double2(A[mt][nt][0], A[mt][nt][1]);
-          if (c + 8 < b)
-            *reinterpret_cast<double2*>(&Yt[y_index(r, c + 8, b)]) = make_double2(A[mt][nt][2], A[mt][nt][3]);
-        }
-      double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
-      for (int idx = tid; idx < b * b; idx += NTC) {
-        const int k = idx % b, j = idx / b;
-        Tt[idx] = k <= j ? sm.Ts[k + BM * j] : 0.0;
-      }
-    }
+    compute_role<4>(sm, P, plan, Yg, Tg, warp_rbase(warp));
   }
   __syncthreads();
   for (int idx = tid; idx < b * b; idx += NT) {
@@ -497,6 +578,15 @@ tsqr_leaf2_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __res
 }
 
 size_t leaf2_smem() { return sizeof(lf2::Smem); }
+
+#ifdef TTB_LF2_CLK
+extern "C" int ttb_dbg_lf2clk(long long* out) {
+  return cudaMemcpyFromSymbol(out, lf2::g_lf2clk, sizeof(long long) * 64 * 8) == cudaSuccess ? 0 : 5;
+}
+extern "C" int ttb_dbg_lf2col(long long* out) {
+  return cudaMemcpyFromSymbol(out, lf2::g_lf2col, sizeof(long long) * 64 * 12) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 void launch_leaf2(Ctx& ctx, const Panel& panel, const LeafPlan& plan, double* Y, double* T, double* Rleaf) {
   smem_attr((const void*)tsqr_leaf2_kernel, sizeof(lf2::Smem));

@@ -662,9 +662,11 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   auto leaf = tsqr_leaf_kernel<LC_>;
   set_smem_attr<LC_>((const void*)leaf);
   {
-    static const bool v1 = getenv("TTB_LEAF_V1") != nullptr;  // A/B switch: the unblocked column pipeline
+    // TTB_LEAF2=1 selects the blocked panel-warp leaf (leaf2.cu): correct, but
+    // measured slower than the column pipeline on B200, so opt-in
+    static const bool v2 = getenv("TTB_LEAF2") != nullptr;
     ProfScope ps("tsqr_leaf", st);
-    if (f.cls == 64 && !v1) {
+    if (f.cls == 64 && v2) {
       launch_leaf2(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
     } else {
       leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
