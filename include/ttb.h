@@ -178,6 +178,18 @@ int ttb_round(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim
               const int64_t* dims, const int64_t* ranks, const double* const* in,
               double* const* out, int64_t* out_ranks, double* meta);
 
+/* Implicit Hadamard-then-round: round_tt(hadamard(x, w)) (ops.py:109-132
+ * then parallel.py:293-438) WITHOUT materialising the Hadamard product --
+ * the rank rx*rw Kronecker slices are formed on the fly where the rounding
+ * reads its input (the first sweep's first TSQR panel and its R-folds; the
+ * paper's suggestion, survey 8(f) row 4).  x[n] / w[n] are
+ * this rank's slabs of the two factors; out[n] is sized by the PRODUCT
+ * ranks rx[n]*rw[n] (the first sweep's folded cores live there), results
+ * packed at the front as in ttb_round. */
+int ttb_round_hadamard(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim,
+                       const int64_t* dims, const int64_t* rx, const int64_t* rw, const double* const* x,
+                       const double* const* w, double* const* out, int64_t* out_ranks, double* meta);
+
 /* ttb_round on HOST-resident cores (the drop-in form of the reference's
  * numpy-level call): in[n] / out[n] are host pointers (out[n] sized by the
  * input ranks, results packed at the front as in ttb_round).  The upload of

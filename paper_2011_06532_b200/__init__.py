@@ -14,7 +14,7 @@ from .comm import (Communicator, DistComm, LocalComm, LocalGroup, SerialComm, de
 from .errors import (BoundsError, CapabilityError, CapacityError, ContractError, DeadlockError,
                      NumericError, ShapeError, TTError)
 from .operator import KroneckerOperator, apply_operator, load_operator, mode2_multiply, save_operator
-from .ops import add, add_n, hadamard, inner_product, norm, pivoted_cholesky, scale
+from .ops import add, add_n, hadamard, inner_product, norm, pivoted_cholesky, round_hadamard, scale
 from .parallel import (ROUNDING_VARIANTS, RoundingOptions, TruncatedSVD, TSQRFactor, distribute, gather,
                        orthonormalize, round_tt, round_tt_host, serial_tt, truncated_svd, tsqr_apply_q,
                        tsqr_factor)
@@ -29,7 +29,7 @@ __all__ = [
     "ShapeError", "TSQRFactor", "TTCore", "TTError", "TTTensor", "TruncatedSVD", "add", "add_n",
     "apply_operator", "block_bounds", "default_comm", "distribute", "empty_cache", "gather", "hadamard", "inner_product", "load_operator",
     "load_tt", "load_tt_dist", "mode2_multiply", "norm", "pivoted_cholesky",
-    "orthonormalize", "random_tt", "round_tt", "round_tt_host", "run_local_ranks", "save_operator", "save_tt",
+    "orthonormalize", "random_tt", "round_hadamard", "round_tt", "round_tt_host", "run_local_ranks", "save_operator", "save_tt",
     "save_tt_dist", "scale", "serial_tt", "truncated_svd", "tsqr_apply_q",
     "tsqr_factor", "__version__",
 ]

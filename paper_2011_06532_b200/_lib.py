@@ -63,6 +63,8 @@ SIGNATURES = {
     "ttb_orthonormalize": (C.c_int, [_P, C.c_int, C.c_int, _PI64, _PI64, _PP, _PP]),
     "ttb_norm_ortho": (C.c_int, [_P, C.c_int, _PI64, _PI64, _PP, _PD]),
     "ttb_round": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PP, _PP, _PI64, _PD]),
+    "ttb_round_hadamard": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PI64, _PP, _PP, _PP,
+                                     _PI64, _PD]),
     "ttb_round_host": (C.c_int, [_P, C.c_int, C.c_double, _I64, C.c_int, _PI64, _PI64, _PP, _PP, _PI64, _PD]),
     "ttb_tsqr_factor": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _PP, _P]),
     "ttb_tsqr_apply": (C.c_int, [_P, _P, _I64, _P, _P]),

@@ -41,6 +41,7 @@ static Panel panel_of(const double* p, int64_t rl, int64_t I, int64_t rr, int tr
   q.I = I;
   q.rr = rr;
   q.trans = trans;
+  q.kron = Kron();
   return q;
 }
 
@@ -444,9 +445,12 @@ struct HostTimer {  // diagnostics: TTB_DEBUG_HOSTTIME prints host-side phase ti
   ~HostTimer() { *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
 };
 
+// kin (optional, ndim entries): the input cores are implicit Hadamard cores
+// (ttb_round_hadamard); they are only ever read by the first sweep's first
+// TSQR panel and its R-folds, which form the Kronecker slices on the fly.
 static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
                        const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks,
-                       double* meta, HostIO* io) {
+                       double* meta, HostIO* io, const Kron* kin = nullptr) {
   check_chain(ndim, dims, ranks);
   static const bool htime = getenv("TTB_DEBUG_HOSTTIME") != nullptr;
   double t_all = 0, t_fac = 0, t_svd = 0, t_app = 0, t_flush = 0, t_norm = 0;
@@ -472,7 +476,8 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
   meta[3] = 0.0;  // zero
   if (N == 1) {
     if (io) io->need(0, ctx.stream);
-    copy_d2d(ctx, out[0], in[0], r[0] * d[0] * r[1]);
+    if (kin) hadamard_core(ctx, kin[0].x, kin[0].rxl, kin[0].rxr, kin[0].w, kin[0].rwl, kin[0].rwr, d[0], out[0]);
+    else copy_d2d(ctx, out[0], in[0], r[0] * d[0] * r[1]);
     for (int n = 0; n <= N; ++n) out_ranks[n] = r[n];
     if (io) io->ready(0, out[0], r[0] * d[0] * r[1], ctx.stream);
     return;
@@ -534,14 +539,17 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
       const double* src = (n == 0) ? in[0] : out[n];
       const int b = (int)r[n + 1];
       if (io && n == 0) io->need(0, ctx.stream);
-      { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 0), facs[n]); }
+      Panel pn = panel_of(src, r[n], d[n], r[n + 1], 0);
+      if (kin && n == 0) pn.kron = kin[0];
+      { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, pn, facs[n]); }
       if (io) io->need(n + 1, ctx.stream);
       if (!implicit) {
         double* eye = make_eye(ctx, b);
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], r[n], d[n], b, 0));
         ctx.free(eye);
       }
-      gemm_small_left(ctx, b, b, d[n + 1] * r[n + 2], facs[n].R, b, false, in[n + 1], out[n + 1], true);
+      gemm_small_left(ctx, b, b, d[n + 1] * r[n + 2], facs[n].R, b, false, kin ? nullptr : in[n + 1], out[n + 1],
+                      true, kin ? &kin[n + 1] : nullptr, d[n + 1]);
       if (!implicit) tsqr_release(ctx, facs[n]);
     }
     last = out[N - 1];
@@ -551,14 +559,17 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
       const double* src = (n == N - 1) ? in[N - 1] : out[n];
       const int b = (int)r[n];
       if (io && n == N - 1) io->need(N - 1, ctx.stream);
-      tsqr_factor(ctx, panel_of(src, r[n], d[n], r[n + 1], 1), facs[n]);
+      Panel pn = panel_of(src, r[n], d[n], r[n + 1], 1);
+      if (kin && n == N - 1) pn.kron = kin[N - 1];
+      tsqr_factor(ctx, pn, facs[n]);
       if (io) io->need(n - 1, ctx.stream);
       if (!implicit) {
         double* eye = make_eye(ctx, b);
         tsqr_apply(ctx, facs[n], eye, b, panel_of(out[n], b, d[n], r[n + 1], 1));
         ctx.free(eye);
       }
-      gemm_small_right(ctx, r[n - 1] * d[n - 1], b, b, in[n - 1], facs[n].R, b, true, out[n - 1], true);
+      gemm_small_right(ctx, r[n - 1] * d[n - 1], b, b, kin ? nullptr : in[n - 1], facs[n].R, b, true, out[n - 1], true,
+                       kin ? &kin[n - 1] : nullptr, d[n - 1]);
       if (!implicit) tsqr_release(ctx, facs[n]);
     }
     last = out[0];
@@ -679,6 +690,30 @@ int ttb_round(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, 
               const int64_t* ranks, const double* const* in, double* const* out, int64_t* out_ranks, double* meta) {
   TTB_TRY_BEGIN
   round_impl(h->c, variant, eps0, max_rank, ndim, dims, ranks, in, out, out_ranks, meta, nullptr);
+  TTB_TRY_END
+}
+
+int ttb_round_hadamard(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int ndim, const int64_t* dims,
+                       const int64_t* rx, const int64_t* rw, const double* const* x, const double* const* w,
+                       double* const* out, int64_t* out_ranks, double* meta) {
+  TTB_TRY_BEGIN
+  check_chain(ndim, dims, rx);
+  check_chain(ndim, dims, rw);
+  TTB_CHECK(x && w && out, TTB_ERR_CONTRACT, "null core pointer array");
+  std::vector<int64_t> r(ndim + 1);
+  std::vector<Kron> kz(ndim);
+  for (int n = 0; n <= ndim; ++n) r[n] = rx[n] * rw[n];
+  for (int n = 0; n < ndim; ++n) {
+    kz[n].x = x[n];
+    kz[n].w = w[n];
+    kz[n].rxl = rx[n];
+    kz[n].rxr = rx[n + 1];
+    kz[n].rwl = rw[n];
+    kz[n].rwr = rw[n + 1];
+  }
+  std::vector<const double*> none(ndim, nullptr);
+  round_impl(h->c, variant, eps0, max_rank, ndim, dims, r.data(), none.data(), out, out_ranks, meta, nullptr,
+             kz.data());
   TTB_TRY_END
 }
 

@@ -31,7 +31,24 @@ struct SkinnyArgs {
   double* O;          // out(m, j) = O[m * osm + j * osj]
   int64_t osm, osj;
   int upper;          // S is upper triangular (S(m, k) = 0 for k < m): the R-folds (dtrmm)
+  // B from an implicit Hadamard core Z (kron.x set, B unused): kmode 1 = H(Z)
+  // (B(k, j) = Z[k, j % I, j / I]), kmode 2 = V(Z)^T (B(k, r) = Z[r % zl, r / zl, k])
+  Kron kron;
+  int kmode = 0;
+  int64_t kI = 0, kzl = 0;
 };
+
+__device__ __forceinline__ double skinny_b(const SkinnyArgs& a, int k, int64_t j) {
+  if (a.kmode == 1) {
+    const int64_t m = j / a.kI;
+    return a.kron.at(k, j - m * a.kI, m, a.kI);
+  }
+  if (a.kmode == 2) {
+    const int64_t i = j / a.kzl;
+    return a.kron.at(j - i * a.kzl, i, k, a.kI);
+  }
+  return __ldg(&a.B[k * a.bsk + j * a.bsj]);
+}
 
 template <int MB>  // M rounded up to MB*8
 __global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
@@ -58,7 +75,7 @@ __global__ void __launch_bounds__(kSkNT) skinny_dmma_kernel(SkinnyArgs a) {
 #pragma unroll
     for (int q = 0; q < kSkMaxK / 4; ++q) {
       const int kb = 4 * q + bk;
-      bf[q] = (jin && kb < a.K) ? __ldg(&a.B[kb * a.bsk + jb * a.bsj]) : 0.0;
+      bf[q] = (jin && kb < a.K) ? skinny_b(a, kb, jb) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < kSkMaxK / 4; ++q) {
@@ -265,8 +282,9 @@ static bool fold_tma(Ctx& ctx, const SkinnyArgs& a) {
 }
 
 // out_H (M x N) = F (M x K) * H (K x N); H col-major ld K, out col-major ld M
+// (kz: H = H(Z) of an implicit Hadamard core with I slices instead of a buffer)
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
-                     double* out, bool upper) {
+                     double* out, bool upper, const Kron* kz, int64_t kI) {
   ProfScope ps("fold_left", ctx.stream);
   SkinnyArgs a;
   a.M = M;
@@ -282,13 +300,20 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
   a.osm = 1;
   a.osj = M;
   a.upper = upper ? 1 : 0;
+  if (kz && kz->x) {  // Z formed on the fly: the generic fragment-loading kernel
+    a.kron = *kz;
+    a.kmode = 1;
+    a.kI = kI;
+    launch_skinny(ctx, a);
+    return;
+  }
   if (getenv("TTB_FOLD_V1") == nullptr && fold_tma<false, 64>(ctx, a)) return;
   launch_skinny(ctx, a);
 }
 
 // out_V (Mb x Nn) = V (Mb x K) * G (K x Nn): computed as out^T = G^T V^T
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
-                      double* out, bool upper) {
+                      double* out, bool upper, const Kron* kz, int64_t kI) {
   ProfScope ps("fold_right", ctx.stream);
   SkinnyArgs a;
   a.M = Nn;
@@ -304,6 +329,14 @@ void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, cons
   a.osm = Mb;
   a.osj = 1;
   a.upper = upper ? 1 : 0;  // S = G^T: upper triangular when G is lower (V R^T)
+  if (kz && kz->x) {
+    a.kron = *kz;
+    a.kmode = 2;
+    a.kI = kI;
+    a.kzl = kz->rxl * kz->rwl;
+    launch_skinny(ctx, a);
+    return;
+  }
   // right fold: K runs per chunk -- wider chunks for small K keep each copy >= 2 KB
   if (getenv("TTB_FOLD_V1") == nullptr && (K <= 16 ? fold_tma<true, 256>(ctx, a) : fold_tma<true, 64>(ctx, a))) return;
   launch_skinny(ctx, a);

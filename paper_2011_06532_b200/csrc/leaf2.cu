@@ -254,6 +254,20 @@ __device__ __forceinline__ void load_tile(double (&A)[NMT][NN][4], const TileIO&
       ok[h] = r < rows;
       off[h] = ok[h] ? io.P.addr(w, io.ia + si, 0) : 0;
     }
+    if (io.P.kron.x) {  // implicit Hadamard core: elements formed on load
+      int si0, w0, si1, w1;
+      tile_row(io.P.trans, rbase + nt * 8 + 2 * t4, io.nsl, io.rs, si0, w0);
+      tile_row(io.P.trans, rbase + nt * 8 + 2 * t4 + 1, io.nsl, io.rs, si1, w1);
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt) {
+        const int c = mt * 16 + g;
+        A[mt][nt][0] = ok[0] && c < b ? io.P.load(w0, io.ia + si0, c) : 0.0;
+        A[mt][nt][1] = ok[1] && c < b ? io.P.load(w1, io.ia + si1, c) : 0.0;
+        A[mt][nt][2] = ok[0] && c + 8 < b ? io.P.load(w0, io.ia + si0, c + 8) : 0.0;
+        A[mt][nt][3] = ok[1] && c + 8 < b ? io.P.load(w1, io.ia + si1, c + 8) : 0.0;
+      }
+      continue;
+    }
 #pragma unroll
     for (int mt = 0; mt < NMT; ++mt) {
       const int c = mt * 16 + g;

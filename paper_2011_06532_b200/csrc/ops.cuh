@@ -31,11 +31,13 @@ void gram_sym_step(Ctx& ctx, double* PL, int* perm, double* Wrec, const double* 
 // gemm.cu: skinny products on unfoldings
 // out_H (M x N) = F (M x K) * H (K x N); col-major, ldH = K, ldOut = M, F ld = ldf (F^T if transF)
 // upper: F is upper triangular (the R-fold, dtrmm) -- zero blocks are skipped
+// kz (optional): H is H(Z) of an implicit Hadamard core with kI slices (H unused)
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
-                     double* out, bool upper = false);
+                     double* out, bool upper = false, const Kron* kz = nullptr, int64_t kI = 0);
 // out_V (Mb x Nn) = V (Mb x K) * G (K x Nn); col-major, ldV = Mb, ldOut = Mb, G ld = ldg (G^T if transG)
 // upper: the effective small operand S(c, k) = G(k, c) is upper triangular (V R^T: transG, G = R)
+// kz (optional): V is V(Z) of an implicit Hadamard core with kI slices (V unused)
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
-                      double* out, bool upper = false);
+                      double* out, bool upper = false, const Kron* kz = nullptr, int64_t kI = 0);
 
 }  // namespace ttb

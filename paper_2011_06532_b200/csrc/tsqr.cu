@@ -57,7 +57,7 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
 #pragma unroll
       for (int u = 0; u < C::CPL; ++u) {
         const int k = col_of<C>(u, warp, lc);
-        A[s][u] = (r < rows && k < b) ? P.base[P.addr(w, ia + si, k)] : 0.0;
+        A[s][u] = (r < rows && k < b) ? P.load(w, ia + si, k) : 0.0;
       }
     }
     zero_G<C>(sm);

@@ -92,14 +92,33 @@ using Tree16 = TCfg<TTB_TREE16, 4>;   // 512 rows: fan-in 32 at b = 16
 //   trans == 0: V(X)    rows per slice rs = rl, columns = rr
 //   trans == 1: H(X)^T  rows per slice rs = rr, columns = rl
 // element (w, i, col) at  V: w + rl*(i + I*col);  H^T: col + rl*(i + I*w)
+// An implicit Hadamard core (ops.py:109-132 layout, never materialised):
+//   Z[a rwl + c, i, b rwr + d] = X[a, i, b] * W[c, i, d]
+// (x == nullptr: no Kronecker source).
+struct Kron {
+  const double* x = nullptr;
+  const double* w = nullptr;
+  int64_t rxl = 0, rxr = 0, rwl = 0, rwr = 0;
+  __device__ __forceinline__ double at(int64_t l, int64_t i, int64_t m, int64_t I) const {
+    const int64_t a = l / rwl, c = l - a * rwl, b = m / rwr, d = m - b * rwr;
+    return __dmul_rn(x[a + rxl * (i + I * b)], w[c + rwl * (i + I * d)]);
+  }
+};
+
 struct Panel {
   double* base;
   int64_t rl, I, rr;
   int trans;
+  Kron kron;  // kron.x set: the panel is a view of an implicit Hadamard core (base unused)
   __host__ __device__ int64_t rs() const { return trans ? rr : rl; }
   __host__ __device__ int64_t ncols() const { return trans ? rl : rr; }
   __host__ __device__ int64_t addr(int64_t w, int64_t i, int64_t col) const {
     return trans ? col + rl * (i + I * w) : w + rl * (i + I * col);
+  }
+  // element (w, i, col) of the view, whatever the source
+  __device__ __forceinline__ double load(int64_t w, int64_t i, int64_t col) const {
+    if (kron.x) return trans ? kron.at(col, i, w, I) : kron.at(w, i, col, I);
+    return base[addr(w, i, col)];
   }
 };
 

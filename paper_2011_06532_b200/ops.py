@@ -141,6 +141,52 @@ def hadamard(x, y, max_rank_product: int | None = None):
     return _to_host(res) if host else res
 
 
+def round_hadamard(x, y, opts, max_rank_product: int | None = None):
+    """round_tt(hadamard(x, y), opts) without materialising the product.
+
+    The product's rank-(rx ry) Kronecker slices (ops.py:109-132) are formed
+    on the fly where the rounding (parallel.py:293-438) reads its input -- the
+    first sweep's first TSQR panel and its R-folds -- instead of being
+    written out and read back (the paper's suggestion).
+    Same result, meta and exceptions as ``round_tt(hadamard(x, y), opts)``;
+    host operands give a host result."""
+    import torch
+
+    from .parallel import _VARIANT_CODE, RoundingOptions
+    from .tensor import f_view
+
+    if not isinstance(opts, RoundingOptions):
+        raise ContractError("round_hadamard expects RoundingOptions")
+    dx, dy, host = _check_pair(x, y)
+    guard = HADAMARD_RANK_GUARD if max_rank_product is None else int(max_rank_product)
+    ranks = tuple(a * b for a, b in zip(dx.ranks, dy.ranks))
+    if max(ranks) > guard:
+        raise CapacityError(f"hadamard bond ranks {max(ranks)} exceed the guard ({guard}); "
+                            "round the operands first or raise max_rank_product")
+    N = dx.ndim
+    ldims = dx.local_dims()
+    flats = [torch.empty(max(1, ranks[n] * ldims[n] * ranks[n + 1]), dtype=torch.float64, device=dx.comm.device)
+             for n in range(N)]
+    out_ranks = (C.c_int64 * (N + 1))()
+    meta = (C.c_double * 4)()
+    _lib.check(_lib.load().ttb_round_hadamard(dx.comm.ctx(), _VARIANT_CODE[opts.variant], float(opts.eps0),
+                                              int(opts.max_rank or 0), N, _lib.i64_array(ldims),
+                                              _lib.i64_array(dx.ranks), _lib.i64_array(dy.ranks), _ptrs(dx.local),
+                                              _ptrs(dy.local), _ptrs(flats), out_ranks, meta))
+    rk = tuple(int(r) for r in out_ranks)
+    slabs = [f_view(flats[n], rk[n], ldims[n], rk[n + 1]) for n in range(N)]
+    md = {"variant": opts.variant, "eps0": opts.eps0, "error_bound_violated": bool(meta[2])}
+    if N > 1:
+        md["norm"] = float(meta[0])
+        if meta[3]:
+            md["zero"] = True
+        else:
+            md["eps_bond"] = float(meta[1])
+            md["output_ranks"] = rk
+    res = DistTTTensor(dx.comm, dx.dims, rk, slabs, md)
+    return _to_host(res) if host else res
+
+
 def inner_product(x, y) -> float:
     """<x, y> by the Gram recurrence, one allreduce per mode (ops.py:135-155)."""
     dx, dy, _ = _check_pair(x, y)
