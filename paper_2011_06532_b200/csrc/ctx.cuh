@@ -73,6 +73,8 @@ struct Tsqr {
   int b = 0, cls = 0;
   Panel panel;
   LeafPlan plan;
+  int wl = 0;    // 1: team-pipelined leaf (wleaf.cu): wplan, Y in 64-row tiles, T holds U = T^{-1}
+  WPlan wplan;
   int ldy = 0, ldy_tree = 0, ftree = 0;
   double *Y = nullptr, *T = nullptr, *Rleaf = nullptr;
   int nloc = 0, nglob = 0;
@@ -92,6 +94,13 @@ struct Tsqr {
 int tsqr_class(int b);
 // blocked (panel warp + fp64 MMA) leaf for 32 < b <= 64 (leaf2.cu)
 void launch_leaf2(Ctx& ctx, const Panel& panel, const LeafPlan& plan, double* Y, double* T, double* Rleaf);
+// team-pipelined leaf and its chain + product apply (wleaf.cu)
+int wleaf_teams(int b);
+size_t wleaf_y_doubles(const WPlan& p);
+size_t wleaf_u_doubles(const WPlan& p);
+void launch_wleaf(Ctx& ctx, const Panel& panel, const WPlan& plan, double* Y, double* U, double* Rleaf);
+void wleaf_apply_tail(Ctx& ctx, const WPlan& plan, const double* Y, const double* U, const double* zin,
+                      const double* D, int k, const Panel& out, double* ubuf, double* z0buf);
 void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f);
 // out (view with k columns, same slicing as the factored panel) = Q [D z; 0]
 void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& out);

@@ -666,7 +666,9 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     // measured slower than the column pipeline on B200, so opt-in
     static const bool v2 = getenv("TTB_LEAF2") != nullptr;
     ProfScope ps("tsqr_leaf", st);
-    if (f.cls == 64 && v2) {
+    if (f.wl) {
+      launch_wleaf(ctx, f.panel, f.wplan, f.Y, f.T, f.Rleaf);
+    } else if (f.cls == 64 && v2) {
       launch_leaf2(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
     } else {
       leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
@@ -707,7 +709,8 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     TTB_LAUNCHED();
     return rin;
   };
-  f.Rlocal = f.nloc > 0 ? run_tree(f.Rleaf, f.plan.G, f.nloc, f.locY, f.locT, f.locR) : f.Rleaf;
+  const int G = f.wl ? f.wplan.G : f.plan.G;
+  f.Rlocal = f.nloc > 0 ? run_tree(f.Rleaf, G, f.nloc, f.locY, f.locT, f.locR) : f.Rleaf;
   if (ctx.nranks > 1) {
     // allgather the rank roots, then a redundant (bitwise identical) tree
     ctx.allgather(f.Rlocal, f.Rstack, (size_t)f.b * f.b);
@@ -740,13 +743,18 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   TTB_CHECK(b >= 1, TTB_ERR_SHAPE, "TSQR needs at least one column");
   TTB_CHECK(f.cls != 0, TTB_ERR_CAPABILITY, "TSQR: column count " + std::to_string(b) + " exceeds 64");
   const int MC = leaf_mc(f.cls), MT = tree_mc(f.cls);
-  TTB_CHECK(rs >= 1 && rs <= MC - b + 1, TTB_ERR_CAPABILITY,
-            "TSQR: rows per slice " + std::to_string(rs) + " too large for the tile (" + std::to_string(MC) + ")");
   const int64_t ns = panel.I;
+  // TTB_WLEAF=1 selects the team-pipelined leaf (wleaf.cu): correct on every
+  // GPU test, but measured no faster than the CTA-wide column pipeline on
+  // the BASELINE panels, so opt-in
+  static const bool wl_on = getenv("TTB_WLEAF") != nullptr;
+  f.wl = wl_on ? 1 : 0;
+  TTB_CHECK(rs >= 1 && (f.wl || rs <= MC - b + 1), TTB_ERR_CAPABILITY,
+            "TSQR: rows per slice " + std::to_string(rs) + " too large for the tile (" + std::to_string(MC) + ")");
   f.plan.nslices = ns;
   f.plan.rs = (int)rs;
   f.plan.b = b;
-  f.plan.ni = (int)(MC / rs);
+  f.plan.ni = (int)std::max<int64_t>(1, MC / rs);
   // CTAs: at most 2 per SM; every CTA gets >= 2 tiles of rows, so small
   // panels are one chain (one head tile = the reference's single dgeqrf
   // pivot order) and the head tile always reaches b rows.
@@ -759,6 +767,20 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   int G = (int)std::min<int64_t>((int64_t)cps * ctx.num_sms, std::max<int64_t>(1, gmax));
   if (ns == 0) G = 1;
   f.plan.G = G;
+  if (f.wl) {
+    // chains: one per SM at most, every team of a chain gets a tile, and
+    // every chain has at least b rows (its head tile is a full QR)
+    const int teams = wleaf_teams(b);
+    const int64_t tiles = (ns * rs + kWH - 1) / kWH;
+    const int64_t per = (b + rs - 1) / rs;  // slices that reach b rows
+    int64_t gw = std::min<int64_t>((int64_t)ctx.num_sms, (tiles + teams - 1) / teams);
+    gw = std::min<int64_t>(gw, ns / per);
+    G = (int)std::max<int64_t>(1, gw);
+    f.wplan.nslices = ns;
+    f.wplan.G = G;
+    f.wplan.rs = (int)rs;
+    f.wplan.b = b;
+  }
   f.ftree = MT / b;
   f.ldy = MC;
   f.ldy_tree = MT;
@@ -784,7 +806,9 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   size_t total = 0;
   auto add = [&](int64_t cnt) { size_t off = total; total += ((size_t)cnt * 8 + 255) / 256 * 256; return off; };
   const int64_t tsz = (bb + 1) & ~1LL;
-  size_t oY = add(ntiles * y_tile_stride(MC, b)), oT = add(ntiles * tsz), oRl = add((int64_t)G * bb);
+  const int64_t nyd = f.wl ? (int64_t)wleaf_y_doubles(f.wplan) : ntiles * y_tile_stride(MC, b);
+  const int64_t ntd = f.wl ? (int64_t)wleaf_u_doubles(f.wplan) : ntiles * tsz;
+  size_t oY = add(nyd), oT = add(ntd), oRl = add((int64_t)G * bb);
   size_t oLY[kMaxLevels], oLT[kMaxLevels], oLR[kMaxLevels];
   for (int L = 0; L < f.nloc; ++L) {
     oLY[L] = add((int64_t)nodes_loc[L] * MT * b);
@@ -828,10 +852,10 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
 
 void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& out) {
   TTB_CHECK(k >= 1 && k <= kApplyKM, TTB_ERR_CAPABILITY, "TSQR apply: k must be in [1, 64]");
-  TTB_CHECK(out.rs() == f.plan.rs && out.I == f.plan.nslices && out.ncols() == k, TTB_ERR_SHAPE,
+  TTB_CHECK(out.rs() == f.panel.rs() && out.I == f.panel.I && out.ncols() == k, TTB_ERR_SHAPE,
             "TSQR apply: output view does not match the factored panel");
-  const int b = f.b, KP = kpad(k), G = f.plan.G;
-  const int64_t bk = (int64_t)b * k, ntiles = f.plan.total_tiles();
+  const int b = f.b, KP = kpad(k), G = f.wl ? f.wplan.G : f.plan.G;
+  const int64_t bk = (int64_t)b * k, ntiles = f.wl ? f.wplan.total_tiles() : f.plan.total_tiles();
   // node counts per level
   std::vector<int> lnodes(f.nloc), gnodes(ctx.nranks > 1 ? f.nglob : 0);
   for (int L = 0, n = G; L < f.nloc; ++L) lnodes[L] = n = (n + f.ftree - 1) / f.ftree;
@@ -872,6 +896,11 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
     Dp = nullptr;
     cur = lev[which];
     which ^= 1;
+  }
+  if (f.wl) {
+    wleaf_apply_tail(ctx, f.wplan, f.Y, f.T, cur, Dp, k, out, ubuf, z0buf);
+    ctx.free(scr);
+    return;
   }
   ChainArgs ca;
   ca.plan = f.plan;

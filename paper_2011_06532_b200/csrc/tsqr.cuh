@@ -159,6 +159,68 @@ struct LeafPlan {
   __host__ __device__ int64_t total_tiles() const { return tile_base(G); }
 };
 
+// Team-pipelined leaf (wleaf.cu): each CTA owns a contiguous run of slices;
+// its rows, in the reference's row order for that run (V: slice-major, as
+// V(X); H^T: mode index fastest over the whole run, as H(X)^T), are cut into
+// tiles of kWH rows regardless of slice boundaries.
+constexpr int kWH = 64;        // tile rows
+constexpr int kWLDY = kWH + 4; // Y column stride inside a tile (= 4 mod 16: conflict-free MMA fragments)
+
+struct WPlan {
+  int64_t nslices;
+  int G;   // CTAs (chains)
+  int rs;  // rows per slice
+  int b;   // columns
+  __host__ __device__ int64_t base() const { return nslices / G; }
+  __host__ __device__ int rem() const { return (int)(nslices % G); }
+  __host__ __device__ int64_t count(int g) const { return base() + (g < rem() ? 1 : 0); }
+  __host__ __device__ int64_t start(int g) const { return (int64_t)g * base() + (g < rem() ? g : rem()); }
+  __host__ __device__ int tiles_of(int64_t cnt) const { return (int)((cnt * rs + kWH - 1) / kWH); }
+  __host__ __device__ int64_t tile_base(int g) const {
+    int64_t t1 = tiles_of(base() + 1), t0 = tiles_of(base());
+    int64_t a = g < rem() ? g : rem();
+    int64_t c = g > rem() ? g - rem() : 0;
+    return a * t1 + c * t0;
+  }
+  __host__ __device__ int64_t total_tiles() const { return tile_base(G); }
+  // chain and tile index of a global tile number
+  __host__ __device__ void tile_of(int64_t tile, int& g, int64_t& t) const {
+    const int64_t t1 = tiles_of(base() + 1), t0 = tiles_of(base());
+    if (tile < (int64_t)rem() * t1) {
+      g = (int)(tile / t1);
+      t = tile - (int64_t)g * t1;
+    } else {
+      const int64_t x = tile - (int64_t)rem() * t1;
+      g = rem() + (int)(x / t0);
+      t = x - (int64_t)(g - rem()) * t0;
+    }
+  }
+};
+// row r of a chain of cnt slices -> (slice offset si, row-in-slice w)
+__host__ __device__ __forceinline__ void wrow(int trans, int64_t r, int64_t cnt, int rs, int64_t& si, int64_t& w) {
+  if (trans) {
+    w = r / cnt;
+    si = r - w * cnt;
+  } else {
+    si = r / rs;
+    w = r - si * rs;
+  }
+}
+// advance (si, w) to the next row of the chain
+__host__ __device__ __forceinline__ void wrow_next(int trans, int64_t cnt, int rs, int64_t& si, int64_t& w) {
+  if (trans) {
+    if (++si == cnt) {
+      si = 0;
+      ++w;
+    }
+  } else {
+    if (++w == rs) {
+      w = 0;
+      ++si;
+    }
+  }
+}
+
 constexpr int kMaxLevels = 12;
 
 // One level of the reduction tree as seen by the apply kernel.
