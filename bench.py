@@ -82,23 +82,37 @@ class Clocks:
         self.enabled = enabled
         self.lines = []
         self.proc = None
+        self.window = None
 
     def __enter__(self):
+        """Start nvidia-smi (20 ms sampling) and wait until it delivers its
+        first sample, so the timed region that follows is covered."""
         if not self.enabled:
             return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
+    def start(self):
+        """Mark the start of the timed region (samples before it are dropped)."""
+        self.window = [time.time(), None]
+
+    def stop(self):
+        if self.window is not None:
+            self.window[1] = time.time()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -111,7 +125,13 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None and self.window[1] is not None:
+            inside = [ln for t, ln in lines if self.window[0] <= t <= self.window[1]]
+            lines = inside if inside else [ln for _, ln in lines[:1]]  # region shorter than one sample
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 6:
                 continue
@@ -205,11 +225,13 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local, enabled=os.environ.get("TTB_BENCH_NO_SMI") is None) as clk:
+        clk.start()
         e0.record(stream)
         for _ in range(args.steps):
             out = T.round_tt(x, opts)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.stop()
     launches = _lib.launch_counter() - l0
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)

@@ -100,6 +100,7 @@ struct TreePlan {
   double* Rrow;               // per node: R rows as they finalise, row-major, ld ldr
   int ldr;
   unsigned* prog;             // per node: NW x finished chunks (zeroed per launch)
+  unsigned* ticket;           // node-id dispenser (zeroed per launch)
 };
 
 constexpr int kMaxChunks = 64;
@@ -255,7 +256,14 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
   unsigned long long* sbar = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(TileSmem<C>) + 127) & ~size_t(127)));
   double* stage = reinterpret_cast<double*>(sbar + kMaxChunks);
-  const int node = blockIdx.x;
+  // node ids come from an atomic ticket in CTA start order, not from
+  // blockIdx: a node only ever waits on children with lower ids, i.e. on
+  // CTAs that already started (and are resident), whatever order the
+  // hardware dispatches the grid in and whatever else shares the SMs
+  __shared__ int node_s;
+  if (threadIdx.x == 0) node_s = (int)atomicAdd(tp.ticket, 1u);
+  __syncthreads();
+  const int node = node_s;
   int L = 0;
   while (L + 1 < tp.nlev && node >= tp.first[L + 1]) ++L;
   const int q = node - tp.first[L];
@@ -700,10 +708,12 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     tp.first[nlev] = total;
     TTB_CHECK(total <= ctx.num_sms, TTB_ERR_CAPABILITY, "TSQR tree: more nodes than SMs");
     tp.prog = f.prog;
+    tp.ticket = f.prog + ctx.num_sms;
     tp.Rrow = f.Rrow;
     tp.ldr = f.ldr;
     TTB_CHECK((f.b + kTreeChunk - 1) / kTreeChunk <= kMaxChunks, TTB_ERR_CAPABILITY, "TSQR tree: too many chunks");
     TTB_CUDA(cudaMemsetAsync(f.prog, 0, sizeof(unsigned) * total, st));
+    TTB_CUDA(cudaMemsetAsync(tp.ticket, 0, sizeof(unsigned), st));
     ProfScope ps("tsqr_tree", st);
     tree<<<total, TC_::NTT, tree_smem<TC_>(), st>>>(tp);
     TTB_LAUNCHED();
@@ -822,7 +832,7 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
     oGT[L] = add((int64_t)nodes_glo[L] * tsz);
     oGR[L] = add((int64_t)nodes_glo[L] * bb);
   }
-  size_t oD = add(b), oR = add(bb), oP = add(ctx.num_sms);
+  size_t oD = add(b), oR = add(bb), oP = add(ctx.num_sms + 1);
   f.ldr = (b + 1) & ~1;
   size_t oRr = add((int64_t)ctx.num_sms * b * f.ldr);
   f.mem = ctx.alloc(total);
