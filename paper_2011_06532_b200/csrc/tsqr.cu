@@ -127,15 +127,15 @@ static __device__ unsigned long long g_tclk[160 * 64];
 extern "C" int ttb_dbg_tclk(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tclk, sizeof(unsigned long long) * 160 * 64) == cudaSuccess ? 0 : 5;
 }
-#define TTB_TSTAMP(idx)                                        \
+#define TTB_TSTAMP(nd, idx)                                    \
   do {                                                         \
     unsigned long long tnow;                                   \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));   \
-    g_tclk[blockIdx.x * 64 + (idx)] = tnow;                    \
+    g_tclk[(nd) * 64 + (idx)] = tnow;                          \
   } while (0)
 #else
-#define TTB_TSTAMP(idx) \
-  do {                  \
+#define TTB_TSTAMP(nd, idx) \
+  do {                      \
   } while (0)
 #endif
 
@@ -159,6 +159,8 @@ struct TreeHooks {
   double* stage;            // shared: MC x ldr
   unsigned long long* sbar; // shared: one per chunk
   int c0, cnt, b, ldr, nchunks;
+  int node;  // debug stamps only
+  double* Rs;  // shared: the node is factored as a body tile [R_child0; children 1..]: child 0 -> Rs
 
   __device__ __forceinline__ unsigned need(int ci) const { return (unsigned)C::NW * (unsigned)(ci + 1); }
   __device__ __forceinline__ void issue(int ci) {
@@ -189,12 +191,21 @@ struct TreeHooks {
   __device__ __forceinline__ void feed(T& A, int j0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lc = lane / C::LR, lr = lane % C::LR;
+    // child 0 goes to Rs, written only by the warp that owns column j0: it
+    // publishes column j0 (and reads its pivot) next, and every other warp
+    // reads Rs rows >= j0 only after that publication's full barrier
     if (!prog_in) {  // complete inputs: everything at the start
       if (j0 > 0) return;
+      if (warp == C::owner_warp(0)) {
+        for (int idx = lane; idx < b * b; idx += 32) {
+          const int r = idx % b, k = idx / b;
+          Rs[r + C::BMAX * k] = r <= k ? Rin[(int64_t)c0 * b * b + idx] : 0.0;
+        }
+      }
 #pragma unroll
       for (int s = 0; s < C::RPL; ++s) {
         const int r = C::row(s, lr);
-        const int ch = r / b, i = r - ch * b;
+        const int ch = r / b + 1, i = r % b;
 #pragma unroll
         for (int t = 0; t < C::CPL; ++t) {
           const int k = col_of<C>(t, warp, lc);
@@ -206,15 +217,21 @@ struct TreeHooks {
     const int ci = j0 / kTreeChunk;
     mbar_wait(&sbar[ci], 0);
     const int j1 = min(j0 + kTreeChunk, b);
+    if (warp == C::owner_warp(j0)) {
+      for (int idx = lane; idx < (j1 - j0) * b; idx += 32) {
+        const int i = j0 + idx / b, k = idx % b;
+        Rs[i + C::BMAX * k] = k >= i ? stage[(int64_t)i * ldr + k] : 0.0;
+      }
+    }
 #pragma unroll
     for (int s = 0; s < C::RPL; ++s) {
       const int r = C::row(s, lr);
-      const int ch = r / b, i = r - ch * b;
+      const int ch = r / b + 1, i = r % b;
       if (ch >= cnt || i < j0 || i >= j1) continue;
 #pragma unroll
       for (int t = 0; t < C::CPL; ++t) {
         const int k = col_of<C>(t, warp, lc);
-        if (k < b) A[s][t] = k >= i ? stage[(int64_t)r * ldr + k] : 0.0;
+        if (k < b) A[s][t] = k >= i ? stage[(int64_t)(ch * b + i) * ldr + k] : 0.0;
       }
     }
   }
@@ -222,21 +239,19 @@ struct TreeHooks {
   __device__ __forceinline__ void post(T& A, int j) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #ifdef TTB_TCLK2
-    if (lane == 0 && warp == 0) TTB_TSTAMP(j);
+    if (lane == 0 && warp == 0) TTB_TSTAMP(node, j);
 #endif
     if (!prog_out) return;
     const int lc = lane / C::LR, lr = lane % C::LR;
-    const int sj = 2 * (j / (2 * C::LR)) + (j & 1), lrj = (j % (2 * C::LR)) / 2;
-    if (lr == lrj) {
+    // row j of R is final in Rs once this warp applied reflector j: the
+    // lr == 0 lane of each column group wrote its columns' entries itself
+    // (update_slot), the diagonal came from the owner group's publish
+    if (lr == 0) {
 #pragma unroll
       for (int t = 0; t < C::CPL; ++t) {
         const int k = col_of<C>(t, warp, lc);
         if (k >= b) continue;
-        double v = 0.0;
-#pragma unroll
-        for (int s = 0; s < C::RPL; ++s)
-          if (C::pivot_slot(s) && s == sj) v = A[s][t];
-        Rrow_out[(int64_t)j * ldr + k] = k >= j ? v : 0.0;
+        Rrow_out[(int64_t)j * ldr + k] = k >= j ? Rs[j + C::BMAX * k] : 0.0;
       }
     }
     if ((j + 1) % kTreeChunk == 0 || j + 1 == b) {
@@ -244,7 +259,7 @@ struct TreeHooks {
       __syncwarp();
       if (lane == 0) atomicAdd(prog_out, 1u);
 #if defined(TTB_TCLK) && !defined(TTB_TCLK_NOCHUNK)
-      if (lane == 0 && warp == 0) TTB_TSTAMP(j / kTreeChunk);
+      if (lane == 0 && warp == 0) TTB_TSTAMP(node, j / kTreeChunk);
 #endif
     }
   }
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
 #ifdef TTB_TCLK
-  if (threadIdx.x == 0) TTB_TSTAMP(63);
+  if (threadIdx.x == 0) TTB_TSTAMP(node, 63);
 #endif
   const bool has_parent = L + 1 < tp.nlev;
   TreeHooks<C> h;
@@ -297,6 +312,8 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   h.b = b;
   h.ldr = tp.ldr;
   h.nchunks = nchunks;
+  h.node = node;
+  h.Rs = sm.Rs;
   // warp specialisation: the extra warpgroup moves the children's rows (one
   // warp of it is enough) and hands its registers to the compute warps, which
   // hold the 256 x 64 register tile
@@ -307,10 +324,31 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-  tile_qr_t<C, true>(A, b, sm, 0, h);
-  store_Y<C>(A, b, true, tp.Y[L] + (int64_t)q * C::MC * b, C::MC);
+  // the stacked triangles as a body tile: [R_child0; R_child1; ...] with
+  // R_child0 in Rs -- reflector j has the support a plain QR of the stack
+  // gives it (row j of child 0, rows <= j of the others), so Y / T are the
+  // same, but the column loop runs the cheaper body path
+  tile_qr_t<C, false>(A, b, sm, 0, h);
+  {
+    double* Yn = tp.Y[L] + (int64_t)q * C::MC * b;
+    for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
+      const int i = idx % b, k = idx / b;
+      Yn[i + (int64_t)C::MC * k] = i == k ? 1.0 : 0.0;  // child 0's block of V: the identity
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lc = lane / C::LR, lr = lane % C::LR;
+#pragma unroll
+    for (int t = 0; t < C::CPL; ++t) {
+      const int k = col_of<C>(t, warp, lc);
+      if (k >= b) continue;
+#pragma unroll
+      for (int s = 0; s < C::RPL; ++s) {
+        const int r = b + C::row(s, lr);
+        if (r < C::MC) Yn[r + (int64_t)C::MC * k] = A[s][t];
+      }
+    }
+  }
   store_T<C>(sm, b, tp.T[L] + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
-  extract_R<C>(A, b, sm);
   C::sync();
   double* Rout = tp.R[L] + (int64_t)q * b * b;
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {

@@ -1,0 +1,6 @@
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 --ignore=tests/test_gpu_fullsize.py > gpurun_out/gt11.log 2>&1
+echo "exit $?" >> gpurun_out/gt11.log
+TTB_LIB=scratch/tclk2.so timeout 120 python tools/treeclk.py 60 8000 60 0 > gpurun_out/tclk11.log 2>&1
+timeout 120 python tools/tsqr_bench.py 60 8000 60 0 60 5 > gpurun_out/tb11.log 2>&1
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-norm > gpurun_out/bench11.log 2>&1
