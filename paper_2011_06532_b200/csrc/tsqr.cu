@@ -45,30 +45,76 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     __syncthreads();
   }
   for (int t = 0; t < ntiles; ++t) {
+    TTB_TILE_CLK(t, 0);
     const int64_t ia = s0 + (int64_t)t * ni;
     const int nsl = (int)min64(ni, n_g - (int64_t)t * ni);
     const int rows = nsl * rs;
-    // load (zero padded)
+    // load (zero padded): one row offset per register row, all loads of the
+    // tile issued back to back (implicit Hadamard panels form elements on load)
+    if (P.kron.x) {
 #pragma unroll
-    for (int s = 0; s < C::RPL; ++s) {
-      const int r = C::row(s, lr);
-      int si, w;
-      tile_row(P.trans, r, nsl, rs, si, w);
+      for (int s = 0; s < C::RPL; ++s) {
+        const int r = C::row(s, lr);
+        int si, w;
+        tile_row(P.trans, r, nsl, rs, si, w);
+#pragma unroll
+        for (int u = 0; u < C::CPL; ++u) {
+          const int k = col_of<C>(u, warp, lc);
+          A[s][u] = (r < rows && k < b) ? P.load(w, ia + si, k) : 0.0;
+        }
+      }
+    } else {
+      const int64_t cst = P.trans ? 1 : P.rl * P.I;
+      int64_t koff[C::CPL];
+      bool kok[C::CPL];
 #pragma unroll
       for (int u = 0; u < C::CPL; ++u) {
         const int k = col_of<C>(u, warp, lc);
-        A[s][u] = (r < rows && k < b) ? P.load(w, ia + si, k) : 0.0;
+        kok[u] = k < b;
+        koff[u] = cst * k;
+      }
+#pragma unroll
+      for (int s = 0; s < C::RPL; ++s) {
+        const int r = C::row(s, lr);
+        int si, w;
+        tile_row(P.trans, r, nsl, rs, si, w);
+        const double* rp = P.base + P.addr(w, ia + si, 0);
+        const bool rok = r < rows;
+#pragma unroll
+        for (int u = 0; u < C::CPL; ++u) A[s][u] = (rok && kok[u]) ? __ldg(rp + koff[u]) : 0.0;
+      }
+    }
+    // pull the next tile's rows into L2 while this one is factored: its load
+    // then waits on L2, not HBM, latency (the runs of a tile are contiguous:
+    // V views one run of rl*nsl doubles per column, H^T views one per row-in-slice)
+    if (t + 1 < ntiles && P.kron.x == nullptr) {
+      const int64_t ia2 = ia + ni;
+      const int nsl2 = (int)min64(ni, n_g - (int64_t)(t + 1) * ni);
+      const int64_t runlen = P.rl * (int64_t)nsl2;  // doubles per run
+      const int nruns = P.trans ? rs : b;
+      const int lines = (int)((runlen * 8 + 127) / 128) + 1;
+      for (int idx = threadIdx.x; idx < nruns * lines; idx += C::NT) {
+        const int q = idx / lines, ln = idx - q * lines;
+        const double* p0 = P.base + P.rl * (ia2 + P.I * (int64_t)q);
+        const char* pl = reinterpret_cast<const char*>(p0) + (int64_t)ln * 128;
+        if (pl < reinterpret_cast<const char*>(p0 + runlen))
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pl));
       }
     }
     zero_G<C>(sm);
     __syncthreads();
+    TTB_TILE_CLK(t, 1);
     const bool head = (t == 0);
     tile_qr<C>(A, b, head, sm, t * b);
+    TTB_TILE_CLK(t, 2);
     const int64_t tile = tb + t;
     store_Y_units<C>(A, b, head, Yg + tile * y_tile_stride(C::MC, b));
-    store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
     if (head) extract_R<C>(A, b, sm);
+    build_T<C>(sm, b);
+    TTB_TILE_CLK(t, 5);
+    store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
     __syncthreads();
+    TTB_TILE_CLK(t, 3);
   }
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
     const int r = idx % b, k = idx / b;
@@ -348,6 +394,7 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
       }
     }
   }
+  build_T<C>(sm, b);
   store_T<C>(sm, b, tp.T[L] + (int64_t)q * (((int64_t)b * b + 1) & ~1LL));
   C::sync();
   double* Rout = tp.R[L] + (int64_t)q * b * b;
@@ -998,6 +1045,11 @@ void tsqr_release(Ctx& ctx, Tsqr& f) {
 
 }  // namespace ttb
 
+#ifdef TTB_DEBUG_TILE
+extern "C" int ttb_dbg_tile(long long* out) {
+  return cudaMemcpyFromSymbol(out, ttb::g_tile_clk, sizeof(long long) * 64 * 8) == cudaSuccess ? 0 : 5;
+}
+#endif
 #ifdef TTB_DEBUG_CLK
 extern "C" int ttb_dbg_clk(long long* out) {
   return cudaMemcpyFromSymbol(out, ttb::g_dclk, sizeof(long long) * 8 * 64 * 8) == cudaSuccess ? 0 : 5;

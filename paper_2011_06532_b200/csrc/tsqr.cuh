@@ -325,37 +325,82 @@ __device__ void init_ring(TileSmem<C>& sm) {
   }
 }
 
-// In-place T = (diag(1/tau) + striu(G))^{-1}, blocked recursive inversion.
-// On entry Gs holds striu(V^T V) (zeros elsewhere) and taus; on exit Gs = T.
+// In-place T = (diag(1/tau) + striu(G))^{-1}.  On entry Gs holds striu(V^T V)
+// (zeros elsewhere) and taus; on exit Gs = T.  The 8 x 8 diagonal blocks are
+// inverted by back substitution (one thread per block column), then the
+// off-diagonal blocks of growing size s = 8, 16, 32 by two fp64 MMA products
+// per block pair, T_AC = -T_AA (U_AC T_CC), skipping the zero halves of the
+// triangular factors.  Seven CTA barriers in all (the previous scalar
+// recursion took twelve plus ~b^3/3 shared-memory FMAs on the SIMT pipe).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <class C>
 __device__ void build_T(TileSmem<C>& sm, int b) {
-  const int tid = threadIdx.x;
   constexpr int BM = C::BMAX;
-  int BP = 1;
+  constexpr int NWARP = C::NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int BP = 8;
   while (BP < b) BP <<= 1;
-  for (int k = tid; k < BP; k += C::NT) sm.Gs[k + BM * k] = (k < b) ? sm.taus[k] : 1.0;
+  const int nbl = BP / 8;
+  // 1. diagonal 8 x 8 blocks: column c of block q (U's diagonal is 1/tau; padded columns: tau = 1)
+  double xcol[8];
+  const bool dthr = tid < nbl * 8;
+  const int q0 = tid >> 3, cq = tid & 7, i0 = q0 * 8;
+  if (dthr) {
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      const int gi = i0 + i;
+      const double tau = gi < b ? sm.taus[gi] : 1.0;
+      double acc = (i == cq) ? 1.0 : 0.0;
+#pragma unroll
+      for (int m = i + 1; m < 8; ++m) acc = fma(-sm.Gs[gi + BM * (i0 + m)], xcol[m], acc);
+      xcol[i] = (i <= cq) ? tau * acc : 0.0;
+    }
+  }
   C::sync();
-  for (int s = 1; s < BP; s <<= 1) {
-    const int nblk = BP / (2 * s);
-    const int items = nblk * s * s;
-    // X = U[A,C] * T[C,C]
-    for (int idx = tid; idx < items; idx += C::NT) {
-      int q = idx / (s * s), rem = idx - q * s * s;
-      int r = rem % s, c = rem / s;
-      int a0 = q * 2 * s, c0 = a0 + s;
-      double acc = 0.0;
-      for (int l = 0; l <= c; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (c0 + l)], sm.Gs[(c0 + l) + BM * (c0 + c)], acc);
-      sm.Xs[idx] = acc;
+  if (dthr) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm.Gs[(i0 + i) + BM * (i0 + cq)] = xcol[i];
+  }
+  C::sync();
+  // 2. off-diagonal blocks, level by level
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int s = 8; s < BP; s <<= 1) {
+    const int tps = s / 8, ntile = (BP / (2 * s)) * tps * tps;
+    // X_q = U_AC T_CC  (T_CC upper: rows k < (tj + 1) 8 of column tile tj)
+    for (int t = warp; t < ntile; t += NWARP) {
+      const int q = t / (tps * tps), rem = t - q * tps * tps, ti = rem % tps, tj = rem / tps;
+      const int a0 = q * 2 * s, c0 = a0 + s;
+      double d0 = 0.0, d1 = 0.0;
+      for (int k0 = 0; k0 < (tj + 1) * 8; k0 += 4) {
+        const double av = sm.Gs[(a0 + ti * 8 + fr) + BM * (c0 + k0 + fc)];
+        const double bv = sm.Gs[(c0 + k0 + fc) + BM * (c0 + tj * 8 + fr)];
+        dmma884(d0, d1, av, bv);
+      }
+      double* X = sm.Xs + q * s * s;
+      const int r = ti * 8 + fr, cc = tj * 8 + 2 * fc;
+      X[r + s * cc] = d0;
+      X[r + s * (cc + 1)] = d1;
     }
     C::sync();
-    // T[A,C] = -T[A,A] * X
-    for (int idx = tid; idx < items; idx += C::NT) {
-      int q = idx / (s * s), rem = idx - q * s * s;
-      int r = rem % s, c = rem / s;
-      int a0 = q * 2 * s, c0 = a0 + s;
-      double acc = 0.0;
-      for (int l = r; l < s; ++l) acc = fma(sm.Gs[(a0 + r) + BM * (a0 + l)], sm.Xs[q * s * s + l + s * c], acc);
-      sm.Gs[(a0 + r) + BM * (c0 + c)] = -acc;
+    // T_AC = -T_AA X_q  (T_AA upper: columns k >= ti 8 of row tile ti)
+    for (int t = warp; t < ntile; t += NWARP) {
+      const int q = t / (tps * tps), rem = t - q * tps * tps, ti = rem % tps, tj = rem / tps;
+      const int a0 = q * 2 * s, c0 = a0 + s;
+      const double* X = sm.Xs + q * s * s;
+      double d0 = 0.0, d1 = 0.0;
+      for (int k0 = ti * 8; k0 < s; k0 += 4) {
+        const double av = sm.Gs[(a0 + ti * 8 + fr) + BM * (a0 + k0 + fc)];
+        const double bv = X[(k0 + fc) + s * (tj * 8 + fr)];
+        dmma884(d0, d1, av, bv);
+      }
+      const int r = ti * 8 + fr, cc = tj * 8 + 2 * fc;
+      sm.Gs[(a0 + r) + BM * (c0 + cc)] = -d0;
+      sm.Gs[(a0 + r) + BM * (c0 + cc + 1)] = -d1;
     }
     C::sync();
   }
@@ -535,6 +580,20 @@ struct NoHooks {
 #endif
 constexpr int kTreeChunk = TTB_TREE_CHUNK;
 
+// Debug-only tile-phase stamps of the leaf (CTA 0, thread 0): build with
+// NVCC_EXTRA=-DTTB_DEBUG_TILE, read back with ttb_dbg_tile.
+#ifdef TTB_DEBUG_TILE
+static __device__ long long g_tile_clk[64 * 8];
+#define TTB_TILE_CLK(t, ph)                                                                  \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 64) g_tile_clk[(t) * 8 + (ph)] = clock64(); \
+  } while (0)
+#else
+#define TTB_TILE_CLK(t, ph) \
+  do {                      \
+  } while (0)
+#endif
+
 template <class C, bool HEAD, class H = NoHooks>
 __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, int gbase, H&& h = H()) {
   constexpr int LR = C::LR, RPL = C::RPL, CPL = C::CPL, BM = C::BMAX;
@@ -640,8 +699,12 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       if (kk[t] < j && lr == 0) sm.Gs[kk[t] + BM * j] = d[t];
     h.post(A, j);
   }
+  TTB_TILE_CLK(gbase / (b > 0 ? b : 1), 4);
   C::sync();
-  build_T<C>(sm, b);
+  // T = (diag(1/tau) + striu(V^T V))^{-1} is formed by the caller (build_T)
+  // after the register tile was stored: the tile's registers are then free
+  // for the MMA fragments (keeping them live across build_T cost the column
+  // loop ~10 % through register pressure)
 }
 
 template <class C>

@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+TTB_LIB=scratch/dtile.so timeout 120 python tools/tileclk.py 60 8000 60 0 > gpurun_out/tile14.log 2>&1
+TTB_LIB=scratch/dtile.so timeout 120 python tools/tileclk.py 60 8000 30 1 >> gpurun_out/tile14.log 2>&1
+timeout 120 python tools/tsqr_bench.py 60 8000 60 0 60 5 > gpurun_out/tb14.log 2>&1
+timeout 120 python tools/tsqr_bench.py 60 8000 30 1 30 5 >> gpurun_out/tb14.log 2>&1
