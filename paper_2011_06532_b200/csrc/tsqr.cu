@@ -44,13 +44,12 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     for (int idx = threadIdx.x; idx < C::BMAX * C::BMAX; idx += C::NT) sm.Rs[idx] = 0.0;
     __syncthreads();
   }
-  for (int t = 0; t < ntiles; ++t) {
-    TTB_TILE_CLK(t, 0);
+  // load tile t (zero padded): one row offset per register row, all loads of
+  // the tile issued back to back (implicit Hadamard panels form elements on load)
+  auto load_tile = [&](int t) {
     const int64_t ia = s0 + (int64_t)t * ni;
     const int nsl = (int)min64(ni, n_g - (int64_t)t * ni);
     const int rows = nsl * rs;
-    // load (zero padded): one row offset per register row, all loads of the
-    // tile issued back to back (implicit Hadamard panels form elements on load)
     if (P.kron.x) {
 #pragma unroll
       for (int s = 0; s < C::RPL; ++s) {
@@ -84,12 +83,18 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
         for (int u = 0; u < C::CPL; ++u) A[s][u] = (rok && kok[u]) ? __ldg(rp + koff[u]) : 0.0;
       }
     }
-    // pull the next tile's rows into L2 while this one is factored: its load
-    // then waits on L2, not HBM, latency (the runs of a tile are contiguous:
-    // V views one run of rl*nsl doubles per column, H^T views one per row-in-slice)
-    if (t + 1 < ntiles && P.kron.x == nullptr) {
-      const int64_t ia2 = ia + ni;
-      const int nsl2 = (int)min64(ni, n_g - (int64_t)(t + 1) * ni);
+  };
+  if (ntiles > 0) load_tile(0);
+  for (int t = 0; t < ntiles; ++t) {
+    TTB_TILE_CLK(t, 0);
+    const int64_t ia = s0 + (int64_t)t * ni;
+    // pull the next-but-one tile's rows into L2 (the next tile's loads are
+    // issued at the end of this one): its load then waits on L2, not HBM
+    // (the runs of a tile are contiguous: V views one run of rl*nsl doubles
+    // per column, H^T views one per row-in-slice)
+    if (t + 2 < ntiles && P.kron.x == nullptr) {
+      const int64_t ia2 = ia + 2 * ni;
+      const int nsl2 = (int)min64(ni, n_g - (int64_t)(t + 2) * ni);
       const int64_t runlen = P.rl * (int64_t)nsl2;  // doubles per run
       const int nruns = P.trans ? rs : b;
       const int lines = (int)((runlen * 8 + 127) / 128) + 1;
@@ -110,6 +115,8 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     const int64_t tile = tb + t;
     store_Y_units<C>(A, b, head, Yg + tile * y_tile_stride(C::MC, b));
     if (head) extract_R<C>(A, b, sm);
+    // the next tile's loads are in flight while T is formed
+    if (t + 1 < ntiles) load_tile(t + 1);
     build_T<C>(sm, b);
     TTB_TILE_CLK(t, 5);
     store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
