@@ -247,13 +247,11 @@ struct TreeHooks {
     // child 0 goes to Rs, written only by the warp that owns column j0: it
     // publishes column j0 (and reads its pivot) next, and every other warp
     // reads Rs rows >= j0 only after that publication's full barrier
-    if (!prog_in) {  // complete inputs: everything at the start
+    if (!prog_in) {  // complete inputs: everything at the start (every compute warp is here)
       if (j0 > 0) return;
-      if (warp == C::owner_warp(0)) {
-        for (int idx = lane; idx < b * b; idx += 32) {
-          const int r = idx % b, k = idx / b;
-          Rs[r + C::BMAX * k] = r <= k ? Rin[(int64_t)c0 * b * b + idx] : 0.0;
-        }
+      for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
+        const int r = idx % b, k = idx / b;
+        Rs[r + C::BMAX * k] = r <= k ? Rin[(int64_t)c0 * b * b + idx] : 0.0;
       }
 #pragma unroll
       for (int s = 0; s < C::RPL; ++s) {
@@ -265,6 +263,7 @@ struct TreeHooks {
           A[s][t] = (ch < cnt && k < b) ? Rin[(int64_t)(c0 + ch) * b * b + i + (int64_t)b * k] : 0.0;
         }
       }
+      C::sync();
       return;
     }
     const int ci = j0 / kTreeChunk;
@@ -308,9 +307,11 @@ struct TreeHooks {
       }
     }
     if ((j + 1) % kTreeChunk == 0 || j + 1 == b) {
-      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");  // release this warp's rows
+      // release this warp's rows: the warp barrier orders every lane's row
+      // stores before lane 0's release-increment (cumulative), which the
+      // parent's acquire-poll pairs with -- no GPU-scope fence per thread
       __syncwarp();
-      if (lane == 0) atomicAdd(prog_out, 1u);
+      if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(prog_out) : "memory");
 #if defined(TTB_TCLK) && !defined(TTB_TCLK_NOCHUNK)
       if (lane == 0 && warp == 0) TTB_TSTAMP(node, j / kTreeChunk);
 #endif
