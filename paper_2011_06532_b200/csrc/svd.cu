@@ -206,12 +206,21 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
           if (valid && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > floor2) {
             // Rutishauser, division-light: t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
             // zeta = (be - al) / (2 ga)  ->  t = s 2|ga| / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
+            // with h = sqrt(dif^2 + 4 ga^2) and den = |dif| + h:
+            // 1 + t^2 = (den^2 + 4 ga^2) / den^2 = 2 h den / den^2, so
+            // cs = den / sqrt(2 h den), sn = sign 2|ga| / sqrt(2 h den):
+            // one sqrt and one rsqrt on the chain instead of sqrt, rcp, rsqrt
+            // (all terms positive: no cancellation)
             const double dif = be - al;
-            const double den = fabs(dif) + sqrt(fma(dif, dif, 4.0 * ga * ga));
-            const double tabs = 2.0 * fabs(ga) * __drcp_rn(den);
-            const double t = ((dif >= 0.0) == (ga >= 0.0)) ? tabs : -tabs;
-            cs = rsqrt(fma(t, t, 1.0));
-            sn = cs * t;
+            const double h = sqrt(fma(dif, dif, 4.0 * ga * ga));
+            const double den = fabs(dif) + h;
+            const double w = rsqrt(2.0 * h * den);
+            cs = den * w;
+            const double sabs = 2.0 * fabs(ga) * w;
+            sn = ((dif >= 0.0) == (ga >= 0.0)) ? sabs : -sabs;
+            // t ga = sign(dif) 2 ga^2 / den and 1 / den = 2 h w^2: no division
+            const double tg0 = 4.0 * ga * ga * h * (w * w);
+            const double tg = dif >= 0.0 ? tg0 : -tg0;
             SVD_CLK(3);
 #pragma unroll
             for (int u = 0; u < kSvdMax / kGrp; ++u) {
@@ -219,8 +228,8 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
               aq[gl + kGrp * u] = sn * xa[u] + cs * ya[u];
             }
             if (gl == 0) {
-              sm.nrm[p] = fma(-t, ga, al);
-              sm.nrm[q] = fma(t, ga, be);
+              sm.nrm[p] = al - tg;
+              sm.nrm[q] = be + tg;
               sm.rotated = 1;
 #ifndef TTB_SVD_NO_EARLY_STOP
               atomicMax(&sm.maxoff, (unsigned long long)__double_as_longlong(ga * ga / (al * be)));
