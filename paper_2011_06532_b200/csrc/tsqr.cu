@@ -143,7 +143,7 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
 // indices than their parents and never wait on them.
 // ------------------------------------------------------------------------
 struct TreePlan {
-  int nlev, b, f;
+  int nlev, b, f, ldy;  // ldy: rows of a node's stored V (= the stack: f * b)
   int first[kMaxLevels + 1];  // global node index of each level's first node
   int n_in[kMaxLevels];       // inputs (children) of each level
   const double* Rin[kMaxLevels];
@@ -368,26 +368,33 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   h.nchunks = nchunks;
   h.node = node;
   h.Rs = sm.Rs;
-  // warp specialisation: the extra warpgroup moves the children's rows (one
-  // warp of it is enough) and hands its registers to the compute warps, which
-  // hold the 256 x 64 register tile
-  static_assert(C::XW == 4 && C::NW % 4 == 0, "whole warpgroups");
-  if (threadIdx.x >= C::NT) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    if (threadIdx.x < C::NT + 32) h.mover();
-    return;
+  // warp specialisation: the extra warp(s) move the children's rows; the
+  // compute warps hold the register tile
+  static_assert(C::XW >= 1, "a data-mover warp");
+  if constexpr (C::XW == 4) {  // a mover warpgroup hands its registers to the compute warps
+    if (threadIdx.x >= C::NT) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+      if (threadIdx.x < C::NT + 32) h.mover();
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  } else {
+    if (threadIdx.x >= C::NT) {
+      if (threadIdx.x < C::NT + 32) h.mover();
+      return;
+    }
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   // the stacked triangles as a body tile: [R_child0; R_child1; ...] with
   // R_child0 in Rs -- reflector j has the support a plain QR of the stack
   // gives it (row j of child 0, rows <= j of the others), so Y / T are the
   // same, but the column loop runs the cheaper body path
   tile_qr_t<C, false>(A, b, sm, 0, h);
   {
-    double* Yn = tp.Y[L] + (int64_t)q * C::MC * b;
+    const int ldy = tp.ldy;
+    double* Yn = tp.Y[L] + (int64_t)q * ldy * b;
     for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
       const int i = idx % b, k = idx / b;
-      Yn[i + (int64_t)C::MC * k] = i == k ? 1.0 : 0.0;  // child 0's block of V: the identity
+      Yn[i + (int64_t)ldy * k] = i == k ? 1.0 : 0.0;  // child 0's block of V: the identity
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lc = lane / C::LR, lr = lane % C::LR;
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
 #pragma unroll
       for (int s = 0; s < C::RPL; ++s) {
         const int r = b + C::row(s, lr);
-        if (r < C::MC) Yn[r + (int64_t)C::MC * k] = A[s][t];
+        if (r < ldy) Yn[r + (int64_t)ldy * k] = A[s][t];
       }
     }
   }
@@ -749,7 +756,8 @@ template <class C>
 size_t tile_smem() { return sizeof(TileSmem<C>); }
 template <class C>
 size_t tree_smem() {
-  return ((sizeof(TileSmem<C>) + 127) & ~size_t(127)) + kMaxChunks * 8 + (size_t)C::MC * C::BMAX * 8;
+  // staging of the children's streamed rows: up to MC / b + 1 children of b rows
+  return ((sizeof(TileSmem<C>) + 127) & ~size_t(127)) + kMaxChunks * 8 + (size_t)(C::MC + C::BMAX) * C::BMAX * 8;
 }
 
 template <class C>
@@ -785,6 +793,7 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     tp.nlev = nlev;
     tp.b = f.b;
     tp.f = f.ftree;
+    tp.ldy = f.ldy_tree;
     int total = 0;
     for (int L = 0; L < nlev; ++L) {
       const int nodes = (n_in + f.ftree - 1) / f.ftree;
@@ -884,9 +893,9 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
     f.wplan.rs = (int)rs;
     f.wplan.b = b;
   }
-  f.ftree = MT / b;
+  f.ftree = MT / b + 1;  // child 0 is the node's shared-memory R, the others fill the register tile
   f.ldy = MC;
-  f.ldy_tree = MT;
+  f.ldy_tree = f.ftree * b;
   // tree sizes
   f.nloc = 0;
   int n = G;
@@ -914,14 +923,14 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
   size_t oY = add(nyd), oT = add(ntd), oRl = add((int64_t)G * bb);
   size_t oLY[kMaxLevels], oLT[kMaxLevels], oLR[kMaxLevels];
   for (int L = 0; L < f.nloc; ++L) {
-    oLY[L] = add((int64_t)nodes_loc[L] * MT * b);
+    oLY[L] = add((int64_t)nodes_loc[L] * f.ldy_tree * b);
     oLT[L] = add((int64_t)nodes_loc[L] * tsz);
     oLR[L] = add((int64_t)nodes_loc[L] * bb);
   }
   size_t oGS = add((int64_t)ctx.nranks * bb);
   size_t oGY[kMaxLevels], oGT[kMaxLevels], oGR[kMaxLevels];
   for (int L = 0; L < f.nglob; ++L) {
-    oGY[L] = add((int64_t)nodes_glo[L] * MT * b);
+    oGY[L] = add((int64_t)nodes_glo[L] * f.ldy_tree * b);
     oGT[L] = add((int64_t)nodes_glo[L] * tsz);
     oGR[L] = add((int64_t)nodes_glo[L] * bb);
   }

@@ -73,7 +73,7 @@ struct TCfg {
 #define TTB_LEAF16 8, 1, 2, 32
 #endif
 #ifndef TTB_TREE64
-#define TTB_TREE64 8, 2, 4, 16
+#define TTB_TREE64 8, 2, 4, 12
 #endif
 #ifndef TTB_TREE32
 #define TTB_TREE32 8, 4, 1, 32
@@ -84,9 +84,19 @@ struct TCfg {
 using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 256 threads (4 columns each), 1 CTA / SM
 using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 512-row tiles, 32 lanes per column
 using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 1024-row tiles, 32 lanes per column
-using Tree64 = TCfg<TTB_TREE64, 4>;   // 256 rows: fan-in 4 at b = 64 (16-lane columns)
-using Tree32 = TCfg<TTB_TREE32, 4>;   // 256 rows: fan-in 8 at b = 32
-using Tree16 = TCfg<TTB_TREE16, 4>;   // 512 rows: fan-in 32 at b = 16
+// Tree nodes: NW compute warps + a data-mover warpgroup.  With 12 warps per
+// SM the register file (16K registers per sub-partition, 3 warps each)
+// allows 168 registers per thread at compile time -- setmaxnreg only moves
+// registers at run time -- so the node's register tile holds the children
+// other than child 0 (which sits in shared memory as the body tile's R):
+// 192 rows at b <= 64 (48 doubles per lane; a 256-row tile spilled and ran
+// ~1.7x slower per column than the leaf's).  Fan-in = MC / b + 1.
+#ifndef TTB_TREE_XW
+#define TTB_TREE_XW 4
+#endif
+using Tree64 = TCfg<TTB_TREE64, TTB_TREE_XW>;   // 192 rows: fan-in 4 at b = 60..64
+using Tree32 = TCfg<TTB_TREE32, TTB_TREE_XW>;   // 256 rows: fan-in 9 at b = 32
+using Tree16 = TCfg<TTB_TREE16, TTB_TREE_XW>;   // 512 rows: fan-in 33 at b = 16
 
 // A row-sliced view of an F-order slab (rl, I, rr):
 //   trans == 0: V(X)    rows per slice rs = rl, columns = rr

@@ -44,3 +44,6 @@ for L in range(len(lv)):
     per = np.array([np.median(np.diff(c[n, :b])) for n in nodes])
     print(f"level {L}: {len(nodes)} nodes  start {st.min():.1f}-{st.max():.1f} us  col0 {first.mean():.1f}  "
           f"done {fin.mean():.1f} (max {fin.max():.1f}) us  median ns/col {np.median(per):.0f}")
+# per-column increments of the first level-0 node (ns)
+n0 = live[0]
+print("node", n0, "col diffs (ns):", np.diff(c[n0, :b]).astype(int).tolist())
