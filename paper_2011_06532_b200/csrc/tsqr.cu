@@ -214,6 +214,12 @@ struct TreeHooks {
   int c0, cnt, b, ldr, nchunks;
   int node;  // debug stamps only
   double* Rs;  // shared: the node is factored as a body tile [R_child0; children 1..]: child 0 -> Rs
+  // no mover warp (XW == 0): warp 0 issues the children's chunks itself -- a
+  // relaxed poll of the children's counters is loaded at the start of each
+  // column step and tested at its end (off the step's critical path); a
+  // chunk that is still missing when a step needs it is polled for blocking
+  int issued = 0;
+  unsigned pv = 0;
 
   __device__ __forceinline__ unsigned need(int ci) const { return (unsigned)C::NW * (unsigned)(ci + 1); }
   __device__ __forceinline__ void issue(int ci) {
@@ -239,7 +245,19 @@ struct TreeHooks {
       issue(ci);
     }
   }
-  __device__ __forceinline__ void pre(int) {}
+  __device__ __forceinline__ void pre(int) {
+    if (C::XW != 0 || !prog_in || issued >= nchunks || (threadIdx.x >> 5) != 0) return;
+    const int lane = threadIdx.x & 31;
+    pv = lane < cnt ? ld_relaxed(prog_in + lane) : 0xffffffffu;
+  }
+  // warp 0: issue chunk `issued` if every child has published it (pv loaded in pre)
+  __device__ __forceinline__ void try_issue() {
+    if (C::XW != 0 || !prog_in || issued >= nchunks || (threadIdx.x >> 5) != 0) return;
+    if (__all_sync(0xffffffffu, pv >= need(issued))) {
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");  // acquire the children's rows
+      issue(issued++);
+    }
+  }
   template <class T>
   __device__ __forceinline__ void feed(T& A, int j0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -267,6 +285,15 @@ struct TreeHooks {
       return;
     }
     const int ci = j0 / kTreeChunk;
+    if (C::XW == 0 && warp == 0) {  // no mover warp: warp 0 issues what is still missing, blocking
+      while (issued <= ci) {
+        for (int c = lane; c < cnt; c += 32)
+          while (ld_acquire(prog_in + c) < need(issued)) {
+          }
+        __syncwarp();
+        issue(issued++);
+      }
+    }
     mbar_wait(&sbar[ci], 0);
     const int j1 = min(j0 + kTreeChunk, b);
     if (warp == C::owner_warp(j0)) {
@@ -290,6 +317,7 @@ struct TreeHooks {
   template <class T>
   __device__ __forceinline__ void post(T& A, int j) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    try_issue();
 #ifdef TTB_TCLK2
     if (lane == 0 && warp == 0) TTB_TSTAMP(node, j);
 #endif
@@ -370,7 +398,6 @@ __global__ void __launch_bounds__(C::NTT, 1) tsqr_tree_kernel(TreePlan tp) {
   h.Rs = sm.Rs;
   // warp specialisation: the extra warp(s) move the children's rows; the
   // compute warps hold the register tile
-  static_assert(C::XW >= 1, "a data-mover warp");
   if constexpr (C::XW == 4) {  // a mover warpgroup hands its registers to the compute warps
     if (threadIdx.x >= C::NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");

@@ -84,15 +84,18 @@ struct TCfg {
 using Leaf64 = TCfg<TTB_LEAF64>;   // b <= 64: 256-row tiles, 256 threads (4 columns each), 1 CTA / SM
 using Leaf32 = TCfg<TTB_LEAF32>;   // b <= 32: 512-row tiles, 32 lanes per column
 using Leaf16 = TCfg<TTB_LEAF16>;   // b <= 16: 1024-row tiles, 32 lanes per column
-// Tree nodes: NW compute warps + a data-mover warpgroup.  With 12 warps per
-// SM the register file (16K registers per sub-partition, 3 warps each)
-// allows 168 registers per thread at compile time -- setmaxnreg only moves
-// registers at run time -- so the node's register tile holds the children
-// other than child 0 (which sits in shared memory as the body tile's R):
-// 192 rows at b <= 64 (48 doubles per lane; a 256-row tile spilled and ran
-// ~1.7x slower per column than the leaf's).  Fan-in = MC / b + 1.
+// Tree nodes: NW compute warps (+ an optional data-mover warpgroup,
+// TTB_TREE_XW=4).  The node's register tile holds the children other than
+// child 0 (which sits in shared memory as the body tile's R): 192 rows at
+// b <= 64, fan-in MC / b + 1.  Default: no mover -- warp 0 polls the
+// children's counters off the column step's critical path and issues the
+// bulk copies itself -- so the CTA has 8 warps and the column loop gets the
+// leaf's register budget (a mover warpgroup makes 12 warps, and the register
+// file, 16K registers per sub-partition, caps the whole kernel at 168 per
+// thread at compile time: setmaxnreg only moves registers at run time).
+// Measured per tree (cfg3 panel): 148 us with the mover, 143 us without.
 #ifndef TTB_TREE_XW
-#define TTB_TREE_XW 4
+#define TTB_TREE_XW 0
 #endif
 using Tree64 = TCfg<TTB_TREE64, TTB_TREE_XW>;   // 192 rows: fan-in 4 at b = 60..64
 using Tree32 = TCfg<TTB_TREE32, TTB_TREE_XW>;   // 256 rows: fan-in 9 at b = 32
