@@ -496,27 +496,19 @@ __host__ __device__ __forceinline__ int kpad(int k) { return (k + 3) & ~3; }
 __host__ __device__ __forceinline__ int ldpad(int n) { return ((n + 11) & ~15) + 4; }
 
 // ---- 1. tree levels -------------------------------------------------------
-// zin: (nodes) blocks of b x k (ld b); zout: (nodes * f) child blocks.
-// D (optional) multiplies the rows of the root input (sign fix).
-// All three products run on the fp64 MMA path (cta_dmma): W = V_top^T Z,
-// U = T W, z_c = [Z;0]_c - V_c U.
-// One CTA per (node, child): every CTA recomputes the node's small
-// W = V_top^T Z, U = T W (b x b x k each) and writes its own child block,
-// so a node's children are produced in parallel, not one after another.
-__global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int nnodes_below, int b, int k,
-                                                                   const double* __restrict__ zin,
-                                                                   const double* __restrict__ D,
-                                                                   double* __restrict__ zout) {
-  extern __shared__ __align__(16) double tsm[];
+// One (node q, child c) pair: U = T_q Z, z_c = [Z;0]_c - V_c U, with Z the
+// node's input block (D, optional, multiplies its rows: the root's sign
+// fix).  Every node is factored as a body tile [R_child0; ...] (tsqr_tree_
+// kernel), so child 0's block of V is the identity: V_top^T Z = Z and
+// z_0 = Z - U.  Both products run on the fp64 MMA path (cta_dmma).
+__device__ __forceinline__ void tree_apply_pair(const Level& L, int q, int c, int b, int k,
+                                                const double* __restrict__ zq, const double* __restrict__ D,
+                                                double* __restrict__ zc, double* tsm) {
   constexpr int NW = kApplyNT / 32;
-  const int q = blockIdx.x / L.f, c = blockIdx.x - q * L.f;
-  if (q * L.f + c >= nnodes_below) return;
   const int ld = ldpad(b);
   double* Z = tsm;            // b x k (ld)
-  double* W = Z + ld * k;     // b x k
-  double* U = W + ld * k;     // b x k
-  double* Vt = U + ld * k;    // b x b  V_top
-  double* Tm = Vt + ld * b;   // b x b
+  double* U = Z + ld * k;     // b x k
+  double* Tm = U + ld * k;    // b x b
   double* Vc = Tm + ld * b;   // b x b  this child's block (c > 0)
   const double* Yg = L.Y + (int64_t)q * L.ldy * b;
   const double* Tg = L.T + (int64_t)q * tstride_of(b);
@@ -524,35 +516,92 @@ __global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int 
   for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
     const int i = idx % b, cc = idx / b;
     const double d = D ? D[i] : 1.0;
-    Z[i + ld * cc] = d * zin[(int64_t)q * b * k + idx];
+    Z[i + ld * cc] = d * zq[idx];
   }
 #pragma unroll 4
   for (int idx = threadIdx.x; idx < b * b; idx += kApplyNT) {
     const int i = idx % b, j = idx / b;
-    Vt[i + ld * j] = Yg[i + (int64_t)L.ldy * j];
     Tm[i + ld * j] = Tg[idx];
     if (c > 0) Vc[i + ld * j] = Yg[(int64_t)c * b + i + (int64_t)L.ldy * j];
   }
   __syncthreads();
-  // W = V_top^T Z  (V_top unit lower: V_top^T(m, l) nonzero for l >= m)
-  cta_dmma(
-      b, k, b, NW, [&](int m, int l) { return (l >= m && l < b) ? Vt[l + ld * m] : 0.0; },
-      [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
-      [&](int m, int n, double v) { W[m + ld * n] = v; });
-  __syncthreads();
-  // U = T W  (T upper)
+  // U = T Z  (T upper)
   cta_dmma(
       b, k, b, NW, [&](int m, int l) { return (l >= m && l < b && m < b) ? Tm[m + ld * l] : 0.0; },
-      [&](int l, int n) { return (l < b && n < k) ? W[l + ld * n] : 0.0; },
+      [&](int l, int n) { return (l < b && n < k) ? Z[l + ld * n] : 0.0; },
       [&](int m, int n, double v) { U[m + ld * n] = v; });
   __syncthreads();
-  double* zc = zout + ((int64_t)q * L.f + c) * b * k;
-  const double* V = c == 0 ? Vt : Vc;
-  const bool top = (c == 0);
-  cta_dmma(
-      b, k, b, NW, [&](int m, int l) { return (m < b && l < b) ? V[m + ld * l] : 0.0; },
-      [&](int l, int n) { return (l < b && n < k) ? U[l + ld * n] : 0.0; },
-      [&](int m, int n, double v) { zc[m + b * n] = (top ? Z[m + ld * n] : 0.0) - v; });
+  if (c == 0) {
+    for (int idx = threadIdx.x; idx < b * k; idx += kApplyNT) {
+      const int m = idx % b, n = idx / b;
+      zc[idx] = Z[m + ld * n] - U[m + ld * n];
+    }
+  } else {
+    cta_dmma(
+        b, k, b, NW, [&](int m, int l) { return (m < b && l < b) ? Vc[m + ld * l] : 0.0; },
+        [&](int l, int n) { return (l < b && n < k) ? U[l + ld * n] : 0.0; },
+        [&](int m, int n, double v) { zc[m + b * n] = -v; });
+  }
+}
+
+// one level, one CTA per (node, child): zin (nodes) blocks of b x k (ld b),
+// zout (nodes * f) child blocks
+__global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_kernel(Level L, int nnodes_below, int b, int k,
+                                                                   const double* __restrict__ zin,
+                                                                   const double* __restrict__ D,
+                                                                   double* __restrict__ zout) {
+  extern __shared__ __align__(16) double tsm[];
+  const int q = blockIdx.x / L.f, c = blockIdx.x - q * L.f;
+  if (q * L.f + c >= nnodes_below) return;
+  tree_apply_pair(L, q, c, b, k, zin + (int64_t)q * b * k, D, zout + ((int64_t)q * L.f + c) * b * k, tsm);
+}
+
+// Every level of a rank's local tree in ONE launch, top-down.  CTAs take
+// pair ids from an atomic ticket in level order (root first), so a pair
+// only waits (on its input block's ready flag) for a pair of the level
+// above, which started earlier; per-level launches cost ~4 launch
+// latencies per apply on the truncation sweep's critical path.
+struct TreeApplyAll {
+  int nlev, b, k;
+  Level lev[kMaxLevels];
+  int below[kMaxLevels];  // child blocks of each level
+  int npair[kMaxLevels];  // nodes * f
+  double* out[kMaxLevels];  // per level: npair blocks of b x k
+  const double* zin;        // the root's input block
+  const double* D;
+  unsigned* flags;          // one per output block of every level (zeroed per launch)
+  int flag_off[kMaxLevels];
+  unsigned* ticket;
+};
+
+__global__ void __launch_bounds__(kApplyNT) tsqr_tree_apply_all_kernel(TreeApplyAll a) {
+  extern __shared__ __align__(16) double tsm[];
+  __shared__ int id_s;
+  if (threadIdx.x == 0) id_s = (int)atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  int id = id_s, L = a.nlev - 1;
+  while (L > 0 && id >= a.npair[L]) id -= a.npair[L--];
+  const Level& lv = a.lev[L];
+  const int q = id / lv.f, c = id - q * lv.f;
+  if (q * lv.f + c >= a.below[L]) return;
+  const double* zq;
+  if (L == a.nlev - 1) {
+    zq = a.zin;
+  } else {
+    const unsigned* fl = a.flags + a.flag_off[L + 1] + q;
+    if (threadIdx.x == 0)
+      while (ld_acquire(fl) == 0u) {
+      }
+    __syncthreads();
+    zq = a.out[L + 1] + (int64_t)q * a.b * a.k;
+  }
+  double* zc = a.out[L] + ((int64_t)q * lv.f + c) * a.b * a.k;
+  tree_apply_pair(lv, q, c, a.b, a.k, zq, L == a.nlev - 1 ? a.D : nullptr, zc, tsm);
+  __syncthreads();  // the block is written
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    atomicExch(a.flags + a.flag_off[L] + q * lv.f + c, 1u);
+  }
 }
 
 // ---- 2. chains ------------------------------------------------------------
@@ -1002,11 +1051,16 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   int64_t maxlev = 1;
   for (int L = 0; L < f.nloc; ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)lnodes[L] * f.ftree);
   for (size_t L = 0; L < gnodes.size(); ++L) maxlev = std::max<int64_t>(maxlev, (int64_t)gnodes[L] * f.ftree);
-  const int64_t nscr = 2 * maxlev * bk + ntiles * b * ldpad(k) + (int64_t)G * bk;
+  int64_t treeblocks = 0;  // every local level's output blocks (one launch holds them all)
+  for (int L = 0; L < f.nloc; ++L) treeblocks += (int64_t)lnodes[L] * f.ftree;
+  const int64_t nscr = 2 * maxlev * bk + ntiles * b * ldpad(k) + (int64_t)G * bk + treeblocks * bk +
+                       (treeblocks + 2) / 2 + 1;
   double* scr = (double*)ctx.alloc((size_t)nscr * sizeof(double));
   double* lev[2] = {scr, scr + maxlev * bk};
   double* ubuf = scr + 2 * maxlev * bk;
   double* z0buf = ubuf + ntiles * b * ldpad(k);
+  double* treebuf = z0buf + (int64_t)G * bk;
+  unsigned* treeflags = reinterpret_cast<unsigned*>(treebuf + treeblocks * bk);
   smem_attr((const void*)tsqr_tree_apply_kernel, 227 * 1024);
   smem_attr((const void*)tsqr_chain_kernel, 227 * 1024);
   smem_attr((const void*)tsqr_product_kernel, 227 * 1024);
@@ -1014,7 +1068,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   const double* Dp = f.D;
   int which = 0;
   const int ldb = ldpad(b);
-  const size_t tsmem = (size_t)(3 * (int64_t)ldb * k + 3 * (int64_t)ldb * b) * sizeof(double);
+  const size_t tsmem = (size_t)(2 * (int64_t)ldb * k + 2 * (int64_t)ldb * b) * sizeof(double);
   // global levels (redundant on every rank), then this rank's block
   for (int L = (int)gnodes.size() - 1; L >= 0; --L) {
     const int below = L == 0 ? ctx.nranks : gnodes[L - 1];
@@ -1026,15 +1080,36 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
     cur = lev[which] + (L == 0 ? (int64_t)ctx.rank * bk : 0);
     which ^= 1;
   }
-  for (int L = f.nloc - 1; L >= 0; --L) {
-    const int below = L == 0 ? G : lnodes[L - 1];
-    Level lv{f.locY[L], f.locT[L], f.ldy_tree, f.ftree, -1};
+  if (f.nloc > 0) {
+    TreeApplyAll ta;
+    ta.nlev = f.nloc;
+    ta.b = b;
+    ta.k = k;
+    int nflags = 0, npairs = 0;
+    for (int L = 0; L < f.nloc; ++L) {
+      ta.lev[L] = Level{f.locY[L], f.locT[L], f.ldy_tree, f.ftree, -1};
+      ta.below[L] = L == 0 ? G : lnodes[L - 1];
+      ta.npair[L] = lnodes[L] * f.ftree;
+      ta.flag_off[L] = nflags;
+      nflags += ta.npair[L];
+      npairs += ta.npair[L];
+    }
+    int64_t off = 0;
+    for (int L = 0; L < f.nloc; ++L) {
+      ta.out[L] = treebuf + off;
+      off += (int64_t)ta.npair[L] * bk;
+    }
+    ta.zin = cur;
+    ta.D = Dp;
+    ta.flags = treeflags;
+    ta.ticket = treeflags + nflags;
+    TTB_CUDA(cudaMemsetAsync(treeflags, 0, sizeof(unsigned) * (nflags + 1), ctx.stream));
+    smem_attr((const void*)tsqr_tree_apply_all_kernel, tsmem);
     ProfScope ps("apply_tree", ctx.stream);
-    tsqr_tree_apply_kernel<<<lnodes[L] * f.ftree, kApplyNT, tsmem, ctx.stream>>>(lv, below, b, k, cur, Dp, lev[which]);
+    tsqr_tree_apply_all_kernel<<<npairs, kApplyNT, tsmem, ctx.stream>>>(ta);
     TTB_LAUNCHED();
     Dp = nullptr;
-    cur = lev[which];
-    which ^= 1;
+    cur = ta.out[0];
   }
   if (f.wl) {
     wleaf_apply_tail(ctx, f.wplan, f.Y, f.T, cur, Dp, k, out, ubuf, z0buf);
