@@ -15,6 +15,18 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// D (16x8) += A (16x8) B (8x8), mma.sync m16n8k8 f64 (4x the work of m8n8k4
+// per instruction).  Fragments (g = lane / 4, t = lane % 4):
+//   A: a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]
+//   B: b0 = B[t][g], b1 = B[t+4][g]
+//   D: d0 = D[g][2t], d1 = D[g][2t+1], d2 = D[g+8][2t], d3 = D[g+8][2t+1]
+__device__ __forceinline__ void dmma_1688(double (&d)[4], double a0, double a1, double a2, double a3, double b0,
+                                          double b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+
 // C(m, n) = sum_{k < K} A(m, k) B(k, n) for m < M, n < N, split in 16x16
 // blocks (2x2 MMA tiles, operand fragments reused twice) over the warps of
 // the CTA.  a(m, k), b(k, n) must return 0 outside [0, M) x [0, K) etc.

@@ -810,15 +810,44 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
     __syncthreads();
     if (rows > 0) {
       double* ob = a.out.base;
-      // Y rows beyond `rows` are exact zeros (zero-padded leaf tiles), so only
-      // the reflector index needs a bound
-      cta_dmma(
-          rows, k, b, NW, [&](int m, int l) { return l < b ? Ys[(m >> 7) * ustride + (m & (kYUnit - 1)) + lys * l] : 0.0; },
-          [&](int l, int n) { return (l < b && n < k) ? Us[l * ldu + n] : 0.0; },
-          [&](int m, int n, double v) {
+      // 16 x 8 output tiles on the m16n8k8 fp64 MMA; Y rows beyond `rows`
+      // are exact zeros (zero-padded leaf tiles), so only the reflector index
+      // needs a bound (columns of u beyond k only feed outputs never stored)
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const int gq = lane >> 2, t4 = lane & 3;
+      const int mt = (rows + 15) >> 4, ntl = (k + 7) >> 3, kst = (b + 7) >> 3;
+      // two output tiles per warp pass share a row tile (the A fragments) and
+      // run as two independent MMA chains (one dependent chain per warp left
+      // the fp64 tensor pipe ~60 % idle)
+      const int ntiles2 = mt * ((ntl + 1) >> 1);
+      for (int tt = warp; tt < ntiles2; tt += NW) {
+        const int m0 = (tt % mt) * 16, n0 = (tt / mt) * 16;
+        const bool two = n0 + 8 < k;
+        const double* ya = Ys + (m0 >> 7) * ustride + (m0 & (kYUnit - 1)) + gq;
+        const double* ub = Us + n0 + gq;
+        double d[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int ks = 0; ks < kst; ++ks) {
+          const int l0 = ks * 8 + t4, l1 = l0 + 4;
+          const bool ok0 = l0 < b, ok1 = l1 < b;
+          const double a0 = ok0 ? ya[lys * l0] : 0.0, a1 = ok0 ? ya[8 + lys * l0] : 0.0;
+          const double a2 = ok1 ? ya[lys * l1] : 0.0, a3 = ok1 ? ya[8 + lys * l1] : 0.0;
+          const double b0 = ok0 ? ub[l0 * ldu] : 0.0, b1 = ok1 ? ub[l1 * ldu] : 0.0;
+          dmma_1688(d, a0, a1, a2, a3, b0, b1);
+          if (two) {
+            const double c0 = ok0 ? ub[l0 * ldu + 8] : 0.0, c1 = ok1 ? ub[l1 * ldu + 8] : 0.0;
+            dmma_1688(e, a0, a1, a2, a3, c0, c1);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + gq + 8 * ((i >> 1) & 1), n = n0 + 8 * (i >> 2) + 2 * t4 + (i & 1);
+          if (m < rows && n < k) {
             const double base = (head && m < b) ? z0[m + b * n] : 0.0;
-            ob[rowoff[m] + cstride * n] = base - v;
-          });
+            ob[rowoff[m] + cstride * n] = base - (i < 4 ? d[i & 3] : e[i & 3]);
+          }
+        }
+      }
     }
     __syncthreads();
   }
