@@ -47,7 +47,13 @@ struct SvdSmem {
   double A[kLd * kSvdMax];   // ld = kLd
   double V[kLd * kSvdMax];
   double nrm[kSvdMax];           // squared column norms, updated with each rotation
-  double rot[2][kSvdMax / 2][2]; // (cs, sn) of each pair of a round (0, 0: none), by round parity
+  // rotation log of a whole sweep, double buffered by sweep parity: the V
+  // side replays sweep s while the A side runs sweep s + 1
+  double rotlog[2][kSvdMax][kSvdMax / 2][2];  // [slot][round][pair] (cs, sn); (0, 0): none
+  int lcmap[2][kSvdMax];                      // the sweep's tournament slot -> column map
+  int lnact[2];
+  int lfinal[2];
+  unsigned long long logfull[2], logempty[2];  // A -> V (count 1), V -> A (count 1)
   double sig[kSvdMax];
   int order[kSvdMax];
   int cmap[kSvdMax];  // tournament slot -> column (>= n: the empty slot)
@@ -64,6 +70,25 @@ __device__ __forceinline__ double grp_sum(double v) {
 #pragma unroll
   for (int off = kGrp / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
+}
+
+// the A-side and V-side thread halves synchronise separately (named barriers)
+__device__ __forceinline__ void bar_half(int id) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(kHalf) : "memory"); }
+__device__ __forceinline__ unsigned svd_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void svd_mbar_init(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(svd_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void svd_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(svd_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void svd_mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done)
+                 : "r"(svd_smem_u32(b)), "r"(parity)
+                 : "memory");
+  } while (!done);
 }
 
 // columns (p, q) of pair pr in round `round` of the circle-method tournament
@@ -99,7 +124,14 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   SvdSmem& sm = *reinterpret_cast<SvdSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const int np = (n + 1) & ~1;  // even number of tournament slots (pad column is zero)
-  if (tid == 0) sm.bad = 0;
+  if (tid == 0) {
+    sm.bad = 0;
+    for (int s2 = 0; s2 < 2; ++s2) {
+      svd_mbar_init(&sm.logfull[s2]);
+      svd_mbar_init(&sm.logempty[s2]);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
   for (int idx = tid; idx < kSvdMax * np; idx += kSvdNT) {
     const int r = idx % kSvdMax, c = idx / kSvdMax;  // rows beyond m stay zero
@@ -118,9 +150,11 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
   const double tol2 = tol * tol;
   const double noise2 = 2.220446049250313e-16 * 2.220446049250313e-16;
   int sweeps = 0;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    // exact squared column norms (one warp per column, A side)
-    if (!vside) {
+  if (!vside) {
+    // ---- A side: the rotation chain, barrier over this half only ----
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      const int slot = sweep & 1;
+      // exact squared column norms (one warp per column)
       for (int c = ltid / 32; c < np; c += kHalf / 32) {
         double acc = 0.0;
         for (int r = ltid % 32; r < m; r += 32) acc = fma(sm.A[r + kLd * c], sm.A[r + kLd * c], acc);
@@ -128,128 +162,152 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if ((ltid % 32) == 0) sm.nrm[c] = acc;
       }
-    }
-    if (tid == 0) {
-      sm.rotated = 0;
-      sm.maxoff = 0ull;
-    }
-    __syncthreads();
-    double nmax = 0.0;
-    for (int c = 0; c < n; ++c) nmax = fmax(nmax, sm.nrm[c]);
-    // pairs of columns that are both negligible are left alone: below
-    // roundoff of the largest column, or so small that all of them together
-    // (<= np * eps^2 * 1e-4 / np) sit inside the discarded tail of the
-    // truncation rule -- their mutual rotations cannot change the kept
-    // factors, the kept rank or the discarded-tail sum (rotations that
-    // involve one non-negligible column are still applied)
-    const double floor2 = fmax(noise2 * nmax, eps * eps * 1e-4 / (double)np);
-    // deflation: at every sweep start, a column whose norm is at or
-    // below the rotation threshold times the largest (4 eps sqrt(m) ||a||max,
-    // e.g. the roundoff columns of a rank-deficient R) leaves the tournament:
-    // by Weyl, skipping its rotations moves every singular value and factor
-    // by at most its norm, the normwise accuracy LAPACK's gesdd itself has.
-    // The live columns keep their index order; an odd count is padded with
-    // an empty slot
-    if (!kSvdDeflate) {
-      for (int c = tid; c < np; c += kSvdNT) sm.cmap[c] = c;
-      if (tid == 0) sm.nact = np;
-    } else if (tid < 32) {
-      int base = 0;
-      for (int c0 = 0; c0 < n; c0 += 32) {
-        const int c = c0 + tid;
-        const bool act = c < n && sm.nrm[c] > tol2 * nmax;
-        const unsigned msk = __ballot_sync(0xffffffffu, act);
-        if (act) sm.cmap[base + __popc(msk & ((1u << tid) - 1u))] = c;
-        base += __popc(msk);
+      if (ltid == 0) {
+        sm.rotated = 0;
+        sm.maxoff = 0ull;
       }
-      if (tid == 0) {
-        if (base & 1) sm.cmap[base] = kSvdMax;
-        sm.nact = base + (base & 1);
+      // the log slot this sweep writes: replayed by the V side two sweeps ago
+      if (sweep >= 2) svd_mbar_wait(&sm.logempty[slot], (unsigned)((sweep >> 1) - 1) & 1u);
+      bar_half(1);
+      double nmax = 0.0;
+      for (int c = 0; c < n; ++c) nmax = fmax(nmax, sm.nrm[c]);
+      // pairs of columns that are both negligible are left alone: below
+      // roundoff of the largest column, or so small that all of them together
+      // (<= np * eps^2 * 1e-4 / np) sit inside the discarded tail of the
+      // truncation rule -- their mutual rotations cannot change the kept
+      // factors, the kept rank or the discarded-tail sum (rotations that
+      // involve one non-negligible column are still applied)
+      const double floor2 = fmax(noise2 * nmax, eps * eps * 1e-4 / (double)np);
+      // deflation: at every sweep start, a column whose norm is at or
+      // below the rotation threshold times the largest (4 eps sqrt(m) ||a||max,
+      // e.g. the roundoff columns of a rank-deficient R) leaves the tournament:
+      // by Weyl, skipping its rotations moves every singular value and factor
+      // by at most its norm, the normwise accuracy LAPACK's gesdd itself has.
+      // The live columns keep their index order; an odd count is padded with
+      // an empty slot
+      if (!kSvdDeflate) {
+        for (int c = ltid; c < np; c += kHalf) sm.lcmap[slot][c] = c;
+        if (ltid == 0) sm.lnact[slot] = np;
+      } else if (ltid < 32) {
+        int base = 0;
+        for (int c0 = 0; c0 < n; c0 += 32) {
+          const int c = c0 + ltid;
+          const bool act = c < n && sm.nrm[c] > tol2 * nmax;
+          const unsigned msk = __ballot_sync(0xffffffffu, act);
+          if (act) sm.lcmap[slot][base + __popc(msk & ((1u << ltid) - 1u))] = c;
+          base += __popc(msk);
+        }
+        if (ltid == 0) {
+          if (base & 1) sm.lcmap[slot][base] = kSvdMax;
+          sm.lnact[slot] = base + (base & 1);
+        }
       }
-    }
-    __syncthreads();
-    const int nt = sm.nact, npairs = nt / 2;
-    for (int round = 0; round <= nt - 1; ++round) {
-      SVD_CLK(0);
-      if (!vside) {
-        if (round < nt - 1) {
-          // one pair slot per group (npairs <= kHalf / kGrp): the whole
-          // warp reaches the shuffles together
-          const int pr = grp;
-          int p = 0, q = 0;
-          const bool live = pr < npairs;
-          if (live) {
-            pair_of(pr, round, nt, p, q);
-            p = sm.cmap[p];
-            q = sm.cmap[q];
-          }
-          const bool valid = live && p < n && q < n;
-          double* ap = sm.A + kLd * p;
-          double* aq = sm.A + kLd * q;
-          double xa[kSvdMax / kGrp], ya[kSvdMax / kGrp];
+      bar_half(1);
+      const int nt = sm.lnact[slot], npairs = nt / 2;
+      const int* cmap = sm.lcmap[slot];
+      for (int round = 0; round < nt - 1; ++round) {
+        SVD_CLK(0);
+        // one pair slot per group (npairs <= kHalf / kGrp): the whole
+        // warp reaches the shuffles together
+        const int pr = grp;
+        int p = 0, q = 0;
+        const bool live = pr < npairs;
+        if (live) {
+          pair_of(pr, round, nt, p, q);
+          p = cmap[p];
+          q = cmap[q];
+        }
+        const bool valid = live && p < n && q < n;
+        double* ap = sm.A + kLd * p;
+        double* aq = sm.A + kLd * q;
+        double xa[kSvdMax / kGrp], ya[kSvdMax / kGrp];
+#pragma unroll
+        for (int u = 0; u < kSvdMax / kGrp; ++u) {
+          xa[u] = valid ? ap[gl + kGrp * u] : 0.0;
+          ya[u] = valid ? aq[gl + kGrp * u] : 0.0;
+        }
+        double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < kSvdMax / kGrp; u += 2) {
+          g0 = fma(xa[u], ya[u], g0);
+          g1 = fma(xa[u + 1], ya[u + 1], g1);
+        }
+        const double al = valid ? sm.nrm[p] : 0.0, be = valid ? sm.nrm[q] : 0.0;
+        SVD_CLK(1);
+        const double ga = grp_sum(g0 + g1);
+        SVD_CLK(2);
+        double cs = 0.0, sn = 0.0;
+        if (valid && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > floor2) {
+          // with h = sqrt(dif^2 + 4 ga^2) and den = |dif| + h:
+          // 1 + t^2 = (den^2 + 4 ga^2) / den^2 = 2 h den / den^2, so
+          // cs = den / sqrt(2 h den), sn = sign 2|ga| / sqrt(2 h den):
+          // one sqrt and one rsqrt on the chain instead of sqrt, rcp, rsqrt
+          // (all terms positive: no cancellation)
+          const double dif = be - al;
+          const double h = sqrt(fma(dif, dif, 4.0 * ga * ga));
+          const double den = fabs(dif) + h;
+          const double w = rsqrt(2.0 * h * den);
+          cs = den * w;
+          const double sabs = 2.0 * fabs(ga) * w;
+          sn = ((dif >= 0.0) == (ga >= 0.0)) ? sabs : -sabs;
+          // t ga = sign(dif) 2 ga^2 / den and 1 / den = 2 h w^2: no division
+          const double tg0 = 4.0 * ga * ga * h * (w * w);
+          const double tg = dif >= 0.0 ? tg0 : -tg0;
+          SVD_CLK(3);
 #pragma unroll
           for (int u = 0; u < kSvdMax / kGrp; ++u) {
-            xa[u] = valid ? ap[gl + kGrp * u] : 0.0;
-            ya[u] = valid ? aq[gl + kGrp * u] : 0.0;
+            ap[gl + kGrp * u] = cs * xa[u] - sn * ya[u];
+            aq[gl + kGrp * u] = sn * xa[u] + cs * ya[u];
           }
-          double g0 = 0.0, g1 = 0.0;
-#pragma unroll
-          for (int u = 0; u < kSvdMax / kGrp; u += 2) {
-            g0 = fma(xa[u], ya[u], g0);
-            g1 = fma(xa[u + 1], ya[u + 1], g1);
-          }
-          const double al = valid ? sm.nrm[p] : 0.0, be = valid ? sm.nrm[q] : 0.0;
-          SVD_CLK(1);
-          const double ga = grp_sum(g0 + g1);
-          SVD_CLK(2);
-          double cs = 0.0, sn = 0.0;
-          if (valid && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > floor2) {
-            // Rutishauser, division-light: t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
-            // zeta = (be - al) / (2 ga)  ->  t = s 2|ga| / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
-            // with h = sqrt(dif^2 + 4 ga^2) and den = |dif| + h:
-            // 1 + t^2 = (den^2 + 4 ga^2) / den^2 = 2 h den / den^2, so
-            // cs = den / sqrt(2 h den), sn = sign 2|ga| / sqrt(2 h den):
-            // one sqrt and one rsqrt on the chain instead of sqrt, rcp, rsqrt
-            // (all terms positive: no cancellation)
-            const double dif = be - al;
-            const double h = sqrt(fma(dif, dif, 4.0 * ga * ga));
-            const double den = fabs(dif) + h;
-            const double w = rsqrt(2.0 * h * den);
-            cs = den * w;
-            const double sabs = 2.0 * fabs(ga) * w;
-            sn = ((dif >= 0.0) == (ga >= 0.0)) ? sabs : -sabs;
-            // t ga = sign(dif) 2 ga^2 / den and 1 / den = 2 h w^2: no division
-            const double tg0 = 4.0 * ga * ga * h * (w * w);
-            const double tg = dif >= 0.0 ? tg0 : -tg0;
-            SVD_CLK(3);
-#pragma unroll
-            for (int u = 0; u < kSvdMax / kGrp; ++u) {
-              ap[gl + kGrp * u] = cs * xa[u] - sn * ya[u];
-              aq[gl + kGrp * u] = sn * xa[u] + cs * ya[u];
-            }
-            if (gl == 0) {
-              sm.nrm[p] = al - tg;
-              sm.nrm[q] = be + tg;
-              sm.rotated = 1;
+          if (gl == 0) {
+            sm.nrm[p] = al - tg;
+            sm.nrm[q] = be + tg;
+            sm.rotated = 1;
 #ifndef TTB_SVD_NO_EARLY_STOP
-              atomicMax(&sm.maxoff, (unsigned long long)__double_as_longlong(ga * ga / (al * be)));
+            atomicMax(&sm.maxoff, (unsigned long long)__double_as_longlong(ga * ga / (al * be)));
 #endif
-            }
-          }
-          if (live && gl == 0) {
-            sm.rot[round & 1][pr][0] = cs;
-            sm.rot[round & 1][pr][1] = sn;
           }
         }
-      } else if (round > 0) {  // V side: the previous round's rotations
-        const int rr = round - 1;
+        if (live && gl == 0) {
+          sm.rotlog[slot][round][pr][0] = cs;
+          sm.rotlog[slot][round][pr][1] = sn;
+        }
+        bar_half(1);
+      }
+      // quadratic convergence: once every rotation of a sweep had
+      // |cos angle(a_p, a_q)| < 1e-9, the next sweep's rotations are of order
+      // 1e-18 -- below the rotation threshold tol ~ 1e-14 -- so that sweep
+      // would only confirm convergence; skip it
+      const int any = sm.rotated;
+      const double maxoff = __longlong_as_double((long long)sm.maxoff);
+      bool stop = !any || sweep == 59;
+#ifndef TTB_SVD_NO_EARLY_STOP
+      stop = stop || maxoff < TTB_SVD_STOP;
+#endif
+      ++sweeps;
+      if (ltid == 0) {
+        sm.lfinal[slot] = stop ? 1 : 0;
+        svd_mbar_arrive(&sm.logfull[slot]);  // release: the log and map of this sweep
+      }
+      bar_half(1);  // every A thread read rotated / maxoff before the next sweep resets them
+      if (stop) break;
+    }
+  } else {
+    // ---- V side: replays each logged sweep one sweep behind, its own barrier ----
+    for (int sweep = 0;; ++sweep) {
+      const int slot = sweep & 1;
+      svd_mbar_wait(&sm.logfull[slot], (unsigned)(sweep >> 1) & 1u);
+      const int nt = sm.lnact[slot], npairs = nt / 2;
+      const int* cmap = sm.lcmap[slot];
+      const bool last = sm.lfinal[slot] != 0;
+      for (int rr = 0; rr < nt - 1; ++rr) {
         for (int pr = grp; pr < npairs; pr += kHalf / kGrp) {
-          const double cs = sm.rot[rr & 1][pr][0], sn = sm.rot[rr & 1][pr][1];
+          const double cs = sm.rotlog[slot][rr][pr][0], sn = sm.rotlog[slot][rr][pr][1];
           if (cs == 0.0) continue;
           int p, q;
           pair_of(pr, rr, nt, p, q);
-          p = sm.cmap[p];
-          q = sm.cmap[q];
+          p = cmap[p];
+          q = cmap[q];
           double* vp = sm.V + kLd * p;
           double* vq = sm.V + kLd * q;
           double xv[kSvdMax / kGrp], yv[kSvdMax / kGrp];
@@ -264,22 +322,13 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
             vq[gl + kGrp * u] = sn * xv[u] + cs * yv[u];
           }
         }
+        bar_half(2);
       }
-      __syncthreads();
+      if (ltid == 0) svd_mbar_arrive(&sm.logempty[slot]);
+      if (last) break;
     }
-    const int any = sm.rotated;
-    // quadratic convergence: once every rotation of a sweep had
-    // |cos angle(a_p, a_q)| < 1e-9, the next sweep's rotations are of order
-    // 1e-18 -- below the rotation threshold tol ~ 1e-14 -- so that sweep
-    // would only confirm convergence; skip it
-    const double maxoff = __longlong_as_double((long long)sm.maxoff);
-    __syncthreads();
-    ++sweeps;
-    if (!any) break;
-#ifndef TTB_SVD_NO_EARLY_STOP
-    if (maxoff < TTB_SVD_STOP) break;
-#endif
   }
+  __syncthreads();
   // singular values
   for (int c = tid / 32; c < n; c += kSvdNT / 32) {
     double acc = 0.0;
