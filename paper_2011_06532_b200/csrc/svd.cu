@@ -60,7 +60,7 @@ struct SvdSmem {
   int nact;           // tournament size of the sweep (even)
   int rotated;
   int bad;
-  unsigned long long maxoff;  // max over the sweep of ga^2 / (al be) (a non-negative double's bits)
+  unsigned long long maxoff;  // 1: some rotation of the sweep had ga^2 >= TTB_SVD_STOP al be
 };
 
 // reduction over the 8 lanes of one pair group (every lane of the warp
@@ -205,6 +205,9 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
       bar_half(1);
       const int nt = sm.lnact[slot], npairs = nt / 2;
       const int* cmap = sm.lcmap[slot];
+      // per-lane sweep flags (published once per sweep, not per rotation:
+      // shared atomics of every pair serialised each round)
+      bool myrot = false, mybig = false;
       for (int round = 0; round < nt - 1; ++round) {
         SVD_CLK(0);
         // one pair slot per group (npairs <= kHalf / kGrp): the whole
@@ -262,11 +265,9 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
           if (gl == 0) {
             sm.nrm[p] = al - tg;
             sm.nrm[q] = be + tg;
-            sm.rotated = 1;
-#ifndef TTB_SVD_NO_EARLY_STOP
-            atomicMax(&sm.maxoff, (unsigned long long)__double_as_longlong(ga * ga / (al * be)));
-#endif
           }
+          myrot = true;
+          mybig |= ga * ga >= TTB_SVD_STOP * (al * be);
         }
         if (live && gl == 0) {
           sm.rotlog[slot][round][pr][0] = cs;
@@ -278,11 +279,13 @@ jacobi_svd_kernel(const double* __restrict__ Ain, int lda, int m, int n, int tra
       // |cos angle(a_p, a_q)| < 1e-9, the next sweep's rotations are of order
       // 1e-18 -- below the rotation threshold tol ~ 1e-14 -- so that sweep
       // would only confirm convergence; skip it
+      if (gl == 0 && myrot) sm.rotated = 1;
+      if (gl == 0 && mybig) sm.maxoff = 1ull;
+      bar_half(1);
       const int any = sm.rotated;
-      const double maxoff = __longlong_as_double((long long)sm.maxoff);
       bool stop = !any || sweep == 59;
 #ifndef TTB_SVD_NO_EARLY_STOP
-      stop = stop || maxoff < TTB_SVD_STOP;
+      stop = stop || sm.maxoff == 0ull;  // no rotation with cos^2 >= TTB_SVD_STOP
 #endif
       ++sweeps;
       if (ltid == 0) {
