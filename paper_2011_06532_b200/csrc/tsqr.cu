@@ -63,24 +63,38 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
         }
       }
     } else {
+      // rows come in pairs (r, r + 1) every 2 LR rows: (slice, row-in-slice)
+      // advances by a constant step, no division per row
       const int64_t cst = P.trans ? 1 : P.rl * P.I;
-      int64_t koff[C::CPL];
-      bool kok[C::CPL];
+      const int per = P.trans ? nsl : rs;  // the fast index wraps at `per`
+      const int step = 2 * C::LR, dq = step / per, dr = step - dq * per;
+      int q0 = (2 * lr) / per, r0 = 2 * lr - q0 * per;  // fast index r0 < per, slow index q0
 #pragma unroll
-      for (int u = 0; u < C::CPL; ++u) {
-        const int k = col_of<C>(u, warp, lc);
-        kok[u] = k < b;
-        koff[u] = cst * k;
-      }
-#pragma unroll
-      for (int s = 0; s < C::RPL; ++s) {
+      for (int s = 0; s < C::RPL; s += 2) {
         const int r = C::row(s, lr);
-        int si, w;
-        tile_row(P.trans, r, nsl, rs, si, w);
-        const double* rp = P.base + P.addr(w, ia + si, 0);
-        const bool rok = r < rows;
 #pragma unroll
-        for (int u = 0; u < C::CPL; ++u) A[s][u] = (rok && kok[u]) ? __ldg(rp + koff[u]) : 0.0;
+        for (int h = 0; h < 2; ++h) {
+          int fq = q0, fr = r0 + h;
+          if (fr == per) {
+            fr = 0;
+            ++fq;
+          }
+          // V: slice = fq, row-in-slice = fr; H^T: row-in-slice (w) = fq, slice = fr
+          const int si = P.trans ? fr : fq, w = P.trans ? fq : fr;
+          const double* rp = P.base + P.addr(w, ia + si, 0);
+          const bool rok = r + h < rows;
+#pragma unroll
+          for (int u = 0; u < C::CPL; ++u) {
+            const int k = col_of<C>(u, warp, lc);
+            A[s + h][u] = (rok && k < b) ? __ldg(rp + cst * k) : 0.0;
+          }
+        }
+        r0 += dr;
+        q0 += dq;
+        if (r0 >= per) {
+          r0 -= per;
+          ++q0;
+        }
       }
     }
   };
