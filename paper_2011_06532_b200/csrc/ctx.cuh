@@ -68,6 +68,8 @@ struct Ctx {
   void sync();
 };
 
+constexpr int kMaxWideBlk = 64;  // column blocks of the general TSQR path (b <= 4096)
+
 // host-side TSQR factor object (see tsqr.cu)
 struct Tsqr {
   int b = 0, cls = 0;
@@ -89,6 +91,13 @@ struct Tsqr {
   double* Rrow = nullptr;    // tree row streams (one b x ldr block per node)
   int ldr = 0;
   void* mem = nullptr;
+  // general path (wide.cu: more than 64 columns, or slices taller than a leaf
+  // tile): explicit orthonormal column blocks wQ (wm x b, col-major, rows in
+  // view memory order), block p = columns [wc0[p], wc0[p+1])
+  int wide = 0, wnblk = 0;
+  int64_t wm = 0;
+  int wc0[kMaxWideBlk + 1];
+  double* wQ = nullptr;
 };
 
 int tsqr_class(int b);

@@ -181,11 +181,14 @@ int ttb_inner(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* rx, cons
   Ctx& ctx = h->c;
   check_chain(ndim, dims, rx);
   check_chain(ndim, dims, ry);
-  double* buf = (double*)ctx.alloc(3 * 64 * 64 * sizeof(double) + 8 * sizeof(int));
+  int64_t wmax = 64 * 64;  // largest carry (ranks above 64 take the general path, wide.cu)
+  for (int n = 0; n <= ndim; ++n) wmax = std::max<int64_t>(wmax, rx[n] * ry[n]);
+  wmax = (wmax + 1) & ~1LL;
+  double* buf = (double*)ctx.alloc((size_t)(3 * wmax) * sizeof(double) + 8 * sizeof(int));
   double* W = buf;
-  double* Wn = buf + 4096;
-  double* Wr = buf + 8192;
-  int* ticket = (int*)(buf + 12288);  // the 16 x 16 kernel's last-CTA reduction
+  double* Wn = buf + wmax;
+  double* Wr = buf + 2 * wmax;
+  int* ticket = (int*)(buf + 3 * wmax);  // the 16 x 16 kernel's last-CTA reduction
   static const double one = 1.0;
   TTB_CUDA(cudaMemcpyAsync(W, &one, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
   TTB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), ctx.stream));
@@ -213,7 +216,13 @@ int ttb_norm_sym(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* ranks
   Ctx& ctx = h->c;
   check_chain(ndim, dims, ranks);
   TTB_CHECK(result && indefinite, TTB_ERR_CONTRACT, "null result");
-  for (int n = 0; n <= ndim; ++n) TTB_CHECK(ranks[n] <= 64, TTB_ERR_CAPABILITY, "norm: ranks above 64");
+  for (int n = 0; n <= ndim; ++n)
+    if (ranks[n] > 64) {
+      // ranks above 64: the symmetric route's pivoted Cholesky of the carry
+      // is a 64 x 64 kernel; the general Gram sweep computes the same <x, x>
+      *indefinite = 0;
+      return ttb_inner(h, ndim, dims, ranks, ranks, in, in, result);
+    }
   double* buf = (double*)ctx.alloc(5 * 64 * 64 * sizeof(double) + 72 * sizeof(int));
   double* W = buf;
   double* Wn = buf + 4096;
@@ -711,6 +720,29 @@ int ttb_round_hadamard(ttb_ctx* h, int variant, double eps0, int64_t max_rank, i
     kz[n].rwl = rw[n];
     kz[n].rwr = rw[n + 1];
   }
+  bool wide = false;
+  for (int n = 0; n <= ndim; ++n) wide |= r[n] > 64;
+  if (wide) {
+    // product ranks above 64 take the general path (wide.cu), which reads
+    // materialised cores: form the Hadamard product once, then round it
+    Ctx& ctx = h->c;
+    std::vector<double*> z(ndim, nullptr);
+    std::vector<const double*> zc(ndim, nullptr);
+    try {
+      for (int n = 0; n < ndim; ++n) {
+        z[n] = (double*)ctx.alloc((size_t)std::max<int64_t>(r[n] * dims[n] * r[n + 1], 1) * sizeof(double));
+        zc[n] = z[n];
+        hadamard_core(ctx, x[n], rx[n], rx[n + 1], w[n], rw[n], rw[n + 1], dims[n], z[n]);
+      }
+      round_impl(ctx, variant, eps0, max_rank, ndim, dims, r.data(), zc.data(), out, out_ranks, meta, nullptr);
+    } catch (...) {
+      for (double* p : z)
+        if (p) ctx.free(p);
+      throw;
+    }
+    for (double* p : z) ctx.free(p);
+    return TTB_OK;
+  }
   std::vector<const double*> none(ndim, nullptr);
   round_impl(h->c, variant, eps0, max_rank, ndim, dims, r.data(), none.data(), out, out_ranks, meta, nullptr,
              kz.data());
@@ -822,7 +854,7 @@ int ttb_truncated_svd(ttb_ctx* h, int64_t m, int64_t n, const double* a, double 
                       double* s, double* v, int64_t* keep, double* tail, int* capped) {
   TTB_TRY_BEGIN
   Ctx& ctx = h->c;
-  TTB_CHECK(m >= 1 && n >= 1 && m <= 64 && n <= 64, TTB_ERR_CAPABILITY, "truncated_svd: 1 <= m, n <= 64");
+  TTB_CHECK(m >= 1 && n >= 1 && m <= 4096 && n <= 4096, TTB_ERR_CAPABILITY, "truncated_svd: 1 <= m, n <= 4096");
   TTB_CHECK(eps >= 0.0, TTB_ERR_CONTRACT, "eps must be nonnegative");
   const bool tall = m >= n;
   const int M = (int)(tall ? m : n), Nn = (int)(tall ? n : m);

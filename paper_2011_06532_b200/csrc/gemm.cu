@@ -13,6 +13,7 @@
 // of 4 it loads one B fragment (streamed from HBM, 32-byte segments) and
 // M/8 A fragments from shared memory.  Every output element is written once.
 #include "ops.cuh"
+#include "wide.cuh"
 #include "prof.cuh"
 #include "dmma.cuh"
 
@@ -285,6 +286,11 @@ static bool fold_tma(Ctx& ctx, const SkinnyArgs& a) {
 // (kz: H = H(Z) of an implicit Hadamard core with I slices instead of a buffer)
 void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf, bool transF, const double* H,
                      double* out, bool upper, const Kron* kz, int64_t kI) {
+  if (M > kSkMaxM || K > kSkMaxK) {  // the general path (wide.cu)
+    TTB_CHECK(!(kz && kz->x), TTB_ERR_CAPABILITY, "fold: implicit Hadamard cores need ranks <= 64");
+    dgemm_strided(ctx, M, N, K, 1.0, F, transF ? ldf : 1, transF ? 1 : ldf, H, 1, K, 0.0, out, 1, M);
+    return;
+  }
   ProfScope ps("fold_left", ctx.stream);
   SkinnyArgs a;
   a.M = M;
@@ -314,6 +320,11 @@ void gemm_small_left(Ctx& ctx, int M, int K, int64_t N, const double* F, int ldf
 // out_V (Mb x Nn) = V (Mb x K) * G (K x Nn): computed as out^T = G^T V^T
 void gemm_small_right(Ctx& ctx, int64_t Mb, int K, int Nn, const double* V, const double* G, int ldg, bool transG,
                       double* out, bool upper, const Kron* kz, int64_t kI) {
+  if (Nn > kSkMaxM || K > kSkMaxK) {  // the general path (wide.cu)
+    TTB_CHECK(!(kz && kz->x), TTB_ERR_CAPABILITY, "fold: implicit Hadamard cores need ranks <= 64");
+    dgemm_strided(ctx, Mb, Nn, K, 1.0, V, 1, Mb, G, transG ? ldg : 1, transG ? 1 : ldg, 0.0, out, 1, Mb);
+    return;
+  }
   ProfScope ps("fold_right", ctx.stream);
   SkinnyArgs a;
   a.M = Nn;

@@ -8,6 +8,7 @@
 // and writes one partial W; a second kernel sums the CTA partials in a
 // fixed order (bitwise deterministic, no atomics).
 #include "ops.cuh"
+#include "wide.cuh"
 #include "prof.cuh"
 
 namespace ttb {
@@ -758,7 +759,10 @@ __global__ void gram_final_kernel(const double* __restrict__ part, int nparts, i
 
 void gram_step(Ctx& ctx, const double* W, const double* X, int64_t ral, int64_t rar, const double* Y, int64_t rbl,
                int64_t rbr, int64_t I, double* Wn, int* ticket) {
-  TTB_CHECK(ral <= 64 && rar <= 64 && rbl <= 64 && rbr <= 64, TTB_ERR_CAPABILITY, "inner product: ranks above 64");
+  if (ral > 64 || rar > 64 || rbl > 64 || rbr > 64) {  // the general path (wide.cu)
+    gram_step_wide(ctx, W, X, ral, rar, Y, rbl, rbr, I, Wn);
+    return;
+  }
   const int64_t cnt = rbr * rar;
   if (I == 0) {
     fill_zero(ctx, Wn, cnt);

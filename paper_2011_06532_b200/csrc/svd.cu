@@ -17,6 +17,7 @@
 #include "ctx.cuh"
 #include "prof.cuh"
 #include "svd.cuh"
+#include "wide.cuh"
 
 namespace ttb {
 
@@ -400,6 +401,10 @@ __global__ void svd_u_kernel(const double* C, const double* s, int m, int keep, 
 
 void jacobi_svd(Ctx& ctx, const double* A, int lda, int m, int n, bool transA, double eps, int max_rank,
                 double* C, double* Vk, double* s, int* info, double* dinfo) {
+  if (m > kSvdMax) {  // the general path (wide.cu)
+    jacobi_svd_wide(ctx, A, lda, m, n, transA, eps, max_rank, C, Vk, s, info, dinfo);
+    return;
+  }
   TTB_CHECK(m >= n && n >= 1 && m <= kSvdMax, TTB_ERR_CAPABILITY, "Jacobi SVD: need 1 <= n <= m <= 64");
   smem_attr((const void*)jacobi_svd_kernel, sizeof(SvdSmem));
   ProfScope ps("jacobi_svd", ctx.stream);

@@ -6,6 +6,7 @@
 #include "ctx.cuh"
 #include "prof.cuh"
 #include "dmma.cuh"
+#include "wide.cuh"
 
 namespace ttb {
 
@@ -966,6 +967,10 @@ static int leaf_mc(int cls) { return cls == 16 ? Leaf16::MC : cls == 32 ? Leaf32
 static int tree_mc(int cls) { return cls == 16 ? Tree16::MC : cls == 32 ? Tree32::MC : Tree64::MC; }
 
 void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
+  if (tsqr_needs_wide(panel)) {  // more than 64 columns or slices taller than a tile: the general path
+    wide_tsqr_factor(ctx, panel, f);
+    return;
+  }
   const int b = (int)panel.ncols();
   const int64_t rs = panel.rs();
   f.b = b;
@@ -1082,6 +1087,10 @@ void tsqr_factor(Ctx& ctx, const Panel& panel, Tsqr& f) {
 }
 
 void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& out) {
+  if (f.wide) {
+    wide_tsqr_apply(ctx, f, z, k, out);
+    return;
+  }
   TTB_CHECK(k >= 1 && k <= kApplyKM, TTB_ERR_CAPABILITY, "TSQR apply: k must be in [1, 64]");
   TTB_CHECK(out.rs() == f.panel.rs() && out.I == f.panel.I && out.ncols() == k, TTB_ERR_SHAPE,
             "TSQR apply: output view does not match the factored panel");
