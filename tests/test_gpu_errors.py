@@ -90,8 +90,10 @@ def test_distribute_rejects_idle_ranks():
 def test_rank_capability_limit():
     """ranks above 64 take the general path (tests/test_gpu_wide.py); the
     remaining limit is 4096 columns per TSQR panel, reported loudly."""
-    x = T.serial_tt(tt((70, 60, 50), (1, 65, 3, 1), 3))
-    assert max(T.round_tt(x, T.RoundingOptions(1e-8)).ranks) <= 60
+    cores = O.random_cores((70, 60, 50), (1, 65, 3, 1), 3)
+    out = T.round_tt(T.serial_tt(T.TTTensor(cores)), T.RoundingOptions(1e-8))
+    ref, _ = O.round_tt(cores, 1e-8, "LRLI")
+    assert tuple(out.ranks) == tuple(O.ranks_of(ref))
     with pytest.raises(T.CapabilityError):
         T.tsqr_factor(np.zeros((10, 4100)))
 
