@@ -103,6 +103,8 @@ struct Tsqr {
 int tsqr_class(int b);
 // blocked (panel warp + fp64 MMA) leaf for 32 < b <= 64 (leaf2.cu)
 void launch_leaf2(Ctx& ctx, const Panel& panel, const LeafPlan& plan, double* Y, double* T, double* Rleaf);
+// row-distributed blocked leaf for 32 < b <= 64 (leaf3.cu)
+void launch_leaf3(Ctx& ctx, const Panel& panel, const LeafPlan& plan, double* Y, double* T, double* Rleaf);
 // team-pipelined leaf and its chain + product apply (wleaf.cu)
 int wleaf_teams(int b);
 size_t wleaf_y_doubles(const WPlan& p);

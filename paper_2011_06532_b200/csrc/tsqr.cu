@@ -894,9 +894,12 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     // TTB_LEAF2=1 selects the blocked panel-warp leaf (leaf2.cu): correct, but
     // measured slower than the column pipeline on B200, so opt-in
     static const bool v2 = getenv("TTB_LEAF2") != nullptr;
+    static const bool v3 = getenv("TTB_LEAF3") != nullptr;
     ProfScope ps("tsqr_leaf", st);
     if (f.wl) {
       launch_wleaf(ctx, f.panel, f.wplan, f.Y, f.T, f.Rleaf);
+    } else if (f.cls == 64 && v3) {
+      launch_leaf3(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
     } else if (f.cls == 64 && v2) {
       launch_leaf2(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
     } else {

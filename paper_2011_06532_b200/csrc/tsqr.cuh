@@ -351,8 +351,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <class C>
-__device__ void build_T(TileSmem<C>& sm, int b) {
+template <class C, class SM = TileSmem<C>>
+__device__ void build_T(SM& sm, int b) {
   constexpr int BM = C::BMAX;
   constexpr int NWARP = C::NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
