@@ -82,6 +82,13 @@ constexpr int NMT = 4;         // m16 column tiles
 constexpr int NN = 4;          // n8 row tiles per warp
 constexpr int NB = 8;          // panel width
 constexpr int WNLD = 12;       // row stride of Wneg (conflict-free A fragments)
+// T formed inside the leaf (cross Gram from the W product + build_T); off: the
+// tile's T is formed from the stored Y by tile_T_kernel, outside the chain
+#ifdef TTB_LF3_NOT
+constexpr bool kInT = false;
+#else
+constexpr bool kInT = true;
+#endif
 
 struct Cfg {
   static constexpr int NT = lf3::NT, BMAX = BM;
@@ -192,9 +199,12 @@ __device__ __forceinline__ double sum8(const double* p) {
 
 // Householder QR of the panel's 8 columns over [pivot rows; tile rows]:
 // HEAD: pivots are tile rows c0 + j (rows above stay R entries); otherwise
-// pivots are rows c0 + j of sm.Rs.  On exit x holds V_p (head: R entries on
-// and above the pivots), sm.taus / sm.Gs (the panel's own Gram entries) and,
-// for chain tiles, the panel block of sm.Rs are updated.
+// pivots are rows c0 + j of sm.Rs.  Finished columns stay RAW in registers
+// during the panel (v_g = scal_g x_g is formed once at the end: no per-step
+// scaling on the column chain).  On exit x holds V_p (head: R entries on and
+// above the pivots), sm.Yb its swizzled copy, sm.taus / sm.Gs the panel's
+// tau and Gram entries v_g . v_J and, for chain tiles, the panel block of
+// sm.Rs is updated.
 template <bool HEAD>
 __device__ __forceinline__ void factor_panel(double (&x)[NN][2], Smem& sm, int c0, int nbp, int rbase) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
@@ -203,6 +213,7 @@ __device__ __forceinline__ void factor_panel(double (&x)[NN][2], Smem& sm, int c
   // (other warps read the old row until then)
   double pend = 0.0;
   int pend_at = -1;
+  double myscal = 0.0, mybeta = 0.0;  // of this lane's own column, once it is factored
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     if (j < nbp) {
@@ -247,79 +258,65 @@ __device__ __forceinline__ void factor_panel(double (&x)[NN][2], Smem& sm, int c
       __syncthreads();
       LF3_STEP(4);
       if (!HEAD && writer && pend_at >= 0) sm.Rs[pend_at] = pend;
-      pend_at = -1;
       const double sig = sum8(&sm.part[buf][0][j]);
       const double sg = sum8(&sm.part[buf][0][g]);
-      const double pvg = HEAD ? sm.pvs[buf][g] : pvg_r;
+      // pivot-row entry of this lane's column: R[J, g] (chain), tile row J (head; a
+      // finished column g < j holds raw x_g there: v_g[J] = scal_g x_g[J])
+      const double pvg = HEAD ? (g < j ? myscal * sm.pvs[buf][g] : sm.pvs[buf][g]) : pvg_r;
       const double alpha = HEAD ? sm.pvs[buf][j] : alpha_r;
       double beta, tau, scal, bv;
       LF3_STEP(5);
       reflector_scalars<false>(alpha, sig, beta, tau, scal, bv);
       LF3_STEP(6);
-      const double d = fma(scal, sg, pvg);
+      // d = v_J . a_g (g > j: the update; g < j with v_g = scal_g x_g: the Gram entry)
+      const double d = fma(scal * (g < j ? myscal : 1.0), sg, pvg);
       const double td = tau * d;
-      if (!HEAD) {
-        // x <- x - cc x_j (g > j), scal x_j (g == j), x (g < j): one fma per element, no divergence
-        const double coef = g > j ? -(td * scal) : (g == j ? scal : 0.0);
+      const double coef = g > j ? -(td * scal) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NN; ++nt) {
+        x[nt][0] = fma(coef, xj[nt][0], x[nt][0]);
+        x[nt][1] = fma(coef, xj[nt][1], x[nt][1]);
+      }
+      if (HEAD && g > j) {  // the pivot row: v_J = 1
 #pragma unroll
         for (int nt = 0; nt < NN; ++nt) {
-          x[nt][0] = fma(coef, xj[nt][0], g == j ? 0.0 : x[nt][0]);
-          x[nt][1] = fma(coef, xj[nt][1], g == j ? 0.0 : x[nt][1]);
+          const int r = rbase + nt * 8 + 2 * t4;
+          if (r == J) x[nt][0] -= td;
+          if (r + 1 == J) x[nt][1] -= td;
         }
+      }
+      if (g == j) {
+        myscal = scal;
+        mybeta = beta;
+      }
+      if (!HEAD) {
         pend = g > j ? pvg - td : beta;
         pend_at = g >= j ? J + BM * (c0 + g) : -1;
-        if (writer) {
-          if (g == j) sm.taus[J] = tau;
-          if (g < j) sm.Gs[(c0 + g) + BM * J] = d;  // v_g . v_J
-        }
-      } else if (g > j) {
-        const double cc = td * scal;
-#pragma unroll
-        for (int nt = 0; nt < NN; ++nt) {
-          x[nt][0] = fma(-cc, xj[nt][0], x[nt][0]);
-          x[nt][1] = fma(-cc, xj[nt][1], x[nt][1]);
-          if (HEAD) {  // the pivot row: v_J = 1
-            const int r = rbase + nt * 8 + 2 * t4;
-            if (r == J) x[nt][0] -= td;
-            if (r + 1 == J) x[nt][1] -= td;
-          }
-        }
-        if (!HEAD) {
-          pend = pvg - td;
-          pend_at = J + BM * (c0 + g);
-        }
-      } else if (g == j) {
-#pragma unroll
-        for (int nt = 0; nt < NN; ++nt) {
-          if (HEAD) {
-            const int r = rbase + nt * 8 + 2 * t4;
-            x[nt][0] = r > J ? xj[nt][0] * scal : (r == J ? beta : x[nt][0]);
-            x[nt][1] = r + 1 > J ? xj[nt][1] * scal : (r + 1 == J ? beta : x[nt][1]);
-          } else {
-            x[nt][0] = xj[nt][0] * scal;
-            x[nt][1] = xj[nt][1] * scal;
-          }
-        }
-        if (writer) sm.taus[J] = tau;
-        if (!HEAD) {
-          pend = beta;
-          pend_at = J + BM * J;
-        }
-      } else {
-        if (writer) sm.Gs[(c0 + g) + BM * J] = d;  // v_g . v_J
+      }
+      if (writer) {
+        if (g == j) sm.taus[J] = tau;
+        if (g < j) sm.Gs[(c0 + g) + BM * J] = d;  // v_g . v_J
       }
       LF3_STEP(7);
     }
   }
-  // V_p -> Yb (head: zeros above the pivot, unit pivot)
+  // v = scal x (head: rows below the pivot; the pivot row takes R's beta), then V_p -> Yb
+  // (head: zeros above the pivot, unit pivot)
 #pragma unroll
   for (int nt = 0; nt < NN; ++nt) {
     const int r = rbase + nt * 8 + 2 * t4;
-    double v0 = x[nt][0], v1 = x[nt][1];
+    double v0, v1;
     if (HEAD) {
       const int Jg = c0 + g;
-      v0 = r < Jg ? 0.0 : (r == Jg ? 1.0 : v0);
-      v1 = r + 1 < Jg ? 0.0 : (r + 1 == Jg ? 1.0 : v1);
+      x[nt][0] = r > Jg ? x[nt][0] * myscal : (r == Jg ? mybeta : x[nt][0]);
+      x[nt][1] = r + 1 > Jg ? x[nt][1] * myscal : (r + 1 == Jg ? mybeta : x[nt][1]);
+      v0 = r < Jg ? 0.0 : (r == Jg ? 1.0 : x[nt][0]);
+      v1 = r + 1 < Jg ? 0.0 : (r + 1 == Jg ? 1.0 : x[nt][1]);
+    } else {
+      x[nt][0] *= myscal;
+      x[nt][1] *= myscal;
+      v0 = x[nt][0];
+      v1 = x[nt][1];
     }
     if (g >= nbp) {
       v0 = 0.0;
@@ -422,7 +419,9 @@ __device__ __forceinline__ void factor_tile(double (&A)[NMT][NN][4], Smem& sm, i
         yw[nt][1] = sm.Yb[bsw(r + 2 * t4 + 1, g)];
       }
 #define LF3_W(MT) wpart_mt<MT>(A, yw, sm)
-      LF3_FOR_MT(mt_all, LF3_W);
+      unsigned wmask = mt_all;
+      if (!kInT) wmask &= ~((1u << ((c0 + NB) >> 4)) - 1);  // trailing m-tiles only
+      LF3_FOR_MT(wmask, LF3_W);
 #undef LF3_W
     }
     __syncthreads();
@@ -445,7 +444,7 @@ __device__ __forceinline__ void factor_tile(double (&A)[NMT][NN][4], Smem& sm, i
         const double wi = __shfl_sync(0xffffffffu, wv, base + i);
         out = fma(sm.Tpp[i * NB + j], wi, out);  // T_pp upper: zero for i > j
       }
-      if (k < c0 && c0 + j < b) sm.Gs[k + BM * (c0 + j)] = raw;
+      if (kInT && k < c0 && c0 + j < b) sm.Gs[k + BM * (c0 + j)] = raw;
       sm.Wneg[k * WNLD + j] = upd ? -out : 0.0;
       if (!HEAD && upd) sm.Rs[(c0 + j) + BM * k] -= out;
     }
@@ -514,7 +513,8 @@ tsqr_leaf3_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __res
         if (pl < reinterpret_cast<const char*>(p0 + runlen)) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pl));
       }
     }
-    for (int k = tid; k < BM * BM; k += lf3::NT) sm.Gs[k] = 0.0;
+    if (lf3::kInT)
+      for (int k = tid; k < BM * BM; k += lf3::NT) sm.Gs[k] = 0.0;
     __syncthreads();
     LF3_CLK(t, 1);
     if (head) lf3::factor_tile<true>(A, sm, b, rbase, t);
@@ -545,12 +545,19 @@ tsqr_leaf3_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __res
       }
     // the next tile's loads are in flight while T is formed
     if (t + 1 < ntiles) lf3::load_tile(A, tile_io(t + 1), b, rbase);
-    build_T<lf3::Cfg>(sm, b);
-    LF3_CLK(t, 8);
-    double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
-    for (int idx = tid; idx < b * b; idx += lf3::NT) {
-      const int k = idx % b, j = idx / b;
-      Tt[idx] = sm.Gs[k + BM * j];
+    if (lf3::kInT) {
+      build_T<lf3::Cfg>(sm, b);
+      LF3_CLK(t, 8);
+      double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
+      for (int idx = tid; idx < b * b; idx += lf3::NT) {
+        const int k = idx % b, j = idx / b;
+        Tt[idx] = sm.Gs[k + BM * j];
+      }
+    } else {
+      LF3_CLK(t, 8);
+      // the tile's tau for tile_T_kernel: the diagonal of the T block
+      double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
+      for (int idx = tid; idx < b; idx += lf3::NT) Tt[idx + b * idx] = sm.taus[idx];
     }
     __syncthreads();
     LF3_CLK(t, 9);
