@@ -308,6 +308,11 @@ void Ctx::sendrecv(int npeers, const int* peers, const double* const* send, cons
 
 void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }
 
+cudaStream_t Ctx::aux_stream() {
+  if (!aux) TTB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  return aux;
+}
+
 cudaStream_t Ctx::side_stream() {
   if (!side) TTB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   return side;
@@ -425,6 +430,7 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
   if (ctx) {
     if (ctx->c.nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->c.nccl_comm);
     if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
+    if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
     if (ctx->c.copy) cudaStreamDestroy(ctx->c.copy);
     if (ctx->c.mapped_host) cudaFreeHost(ctx->c.mapped_host);
     if (ctx->c.dflag) cudaFree(ctx->c.dflag);
@@ -446,6 +452,7 @@ int ttb_ctx_trim(ttb_ctx* ctx) {
   ctx->c.collect(true);
   TTB_CUDA(cudaStreamSynchronize(ctx->c.stream));
   if (ctx->c.side) TTB_CUDA(cudaStreamSynchronize(ctx->c.side));
+  if (ctx->c.aux) TTB_CUDA(cudaStreamSynchronize(ctx->c.aux));
   cudaMemPool_t pool;
   TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
   TTB_CUDA(cudaMemPoolTrimTo(pool, 0));

@@ -31,6 +31,8 @@ struct Ctx {
   cudaStream_t side = nullptr;  // second stream for off-critical-path work (lazily created)
 
   cudaStream_t side_stream();
+  cudaStream_t aux = nullptr;   // third stream: per-tile T factors of a TSQR, formed beside the tree (lazily created)
+  cudaStream_t aux_stream();
   cudaStream_t copy = nullptr;  // host<->device transfers of the host API (lazily created)
   cudaStream_t copy_stream();
   // small device -> host reads (ranks, norms) go through mapped pinned
@@ -87,6 +89,9 @@ struct Tsqr {
   const double* Rraw = nullptr;
   double* D = nullptr;  // sign fix (b)
   double* R = nullptr;  // final sign-fixed R (b x b, col-major), replicated
+  // leaf T factors formed by tile_T_kernel on the aux stream: consumers of T
+  // (the chain apply) and the release of mem wait on this event
+  cudaEvent_t t_ready = nullptr;
   unsigned* prog = nullptr;  // tree progress counters (one per node)
   double* Rrow = nullptr;    // tree row streams (one b x ldr block per node)
   int ldr = 0;

@@ -622,6 +622,10 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     if (io) io->ready(pend.n, pend.out.base, pend.count, sctx.stream);
     ctx.free_after(pend.f2.mem, sctx.stream);  // returned to the pool on the main stream
     pend.f2.mem = nullptr;
+    if (pend.f2.t_ready) {  // the apply above waited on it
+      cudaEventDestroy(pend.f2.t_ready);
+      pend.f2.t_ready = nullptr;
+    }
     ctx.free_after(pend.so.mem, sctx.stream);
     pend.on = false;
   };

@@ -1,5 +1,6 @@
 // TSQR kernels (leaf chain, tree nodes, apply) and the host-side factor object.
 // See tsqr.cuh for the decomposition.  Reference: ttpar tsqr.py:103-327.
+#include <string>
 #include <vector>
 
 #include "tsqr.cuh"
@@ -28,7 +29,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
 tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __restrict__ Tg,
-                 double* __restrict__ Rleaf) {
+                 double* __restrict__ Rleaf, int defer_T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
   const int g = blockIdx.x;
@@ -132,15 +133,59 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     if (head) extract_R<C>(A, b, sm);
     // the next tile's loads are in flight while T is formed
     if (t + 1 < ntiles) load_tile(t + 1);
-    build_T<C>(sm, b);
-    TTB_TILE_CLK(t, 5);
-    store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
+    if (defer_T) {
+      // T is formed outside the chain (tile_T_kernel, beside the tree): hand
+      // over striu(V^T V) with tau on the diagonal
+      TTB_TILE_CLK(t, 5);
+      double* Tt = Tg + tile * (((int64_t)b * b + 1) & ~1LL);
+      for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
+        const int k = idx % b, j = idx / b;
+        Tt[idx] = k < j ? sm.Gs[k + C::BMAX * j] : (k == j ? sm.taus[j] : 0.0);
+      }
+    } else {
+      build_T<C>(sm, b);
+      TTB_TILE_CLK(t, 5);
+      store_T<C>(sm, b, Tg + tile * (((int64_t)b * b + 1) & ~1LL));
+    }
     __syncthreads();
     TTB_TILE_CLK(t, 3);
   }
   for (int idx = threadIdx.x; idx < b * b; idx += C::NT) {
     const int r = idx % b, k = idx / b;
     Rleaf[(int64_t)g * b * b + idx] = sm.Rs[r + C::BMAX * k];
+  }
+}
+
+// ------------------------------------------------------------------------
+// Per-tile T = (diag(1/tau) + striu(V^T V))^{-1} outside the leaf chain: the
+// leaf hands over striu(V^T V) with tau on the diagonal (defer_T); one CTA
+// per tile inverts it in place.  Launched on the aux stream, it runs beside
+// the tree (a latency chain on a third of the SMs) instead of inside every
+// chain's critical path.
+// ------------------------------------------------------------------------
+struct TCfg256 {
+  static constexpr int NT = 256, BMAX = 64;
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+struct TSmem {
+  double Gs[64 * 64];
+  double Xs[64 * 64 / 2];
+  double taus[64];
+};
+__global__ void __launch_bounds__(256) tile_T_kernel(double* __restrict__ Tg, int b, int64_t tsz) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TSmem& sm = *reinterpret_cast<TSmem*>(smem_raw);
+  double* Tt = Tg + (int64_t)blockIdx.x * tsz;
+  for (int idx = threadIdx.x; idx < 64 * 64; idx += 256) {
+    const int k = idx & 63, j = idx >> 6;
+    sm.Gs[idx] = (k < j && j < b) ? Tt[k + b * j] : 0.0;
+  }
+  if (threadIdx.x < b) sm.taus[threadIdx.x] = Tt[threadIdx.x + b * threadIdx.x];
+  __syncthreads();
+  build_T<TCfg256>(sm, b);
+  for (int idx = threadIdx.x; idx < b * b; idx += 256) {
+    const int k = idx % b, j = idx / b;
+    Tt[idx] = sm.Gs[k + 64 * j];
   }
 }
 
@@ -890,6 +935,8 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   cudaStream_t st = ctx.stream;
   auto leaf = tsqr_leaf_kernel<LC_>;
   set_smem_attr<LC_>((const void*)leaf);
+  bool deferred_T = false;
+  cudaEvent_t leaf_done = nullptr;
   {
     // TTB_LEAF2=1 selects the blocked panel-warp leaf (leaf2.cu): correct, but
     // measured slower than the column pipeline on B200, so opt-in
@@ -903,8 +950,16 @@ void run_factor(Ctx& ctx, Tsqr& f) {
     } else if (f.cls == 64 && v2) {
       launch_leaf2(ctx, f.panel, f.plan, f.Y, f.T, f.Rleaf);
     } else {
-      leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf);
+      // TTB_LEAF_T=defer moves build_T out of the chain into tile_T_kernel on the
+      // aux stream (measured: leaf 12.55 -> 11.93 ms per cfg3 round, but the
+      // ~1.0 ms of T blocks slow whatever they run beside by as much -- the
+      // tree when enqueued before it, the R-fold and the SVD when after --
+      // so the step stays at 20.5 ms: opt-in)
+      static const bool dfr = getenv("TTB_LEAF_T") && std::string(getenv("TTB_LEAF_T")) == "defer";
+      const int defer = dfr ? 1 : 0;
+      leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf, defer);
       TTB_LAUNCHED();
+      deferred_T = defer != 0;
     }
   }
   auto tree = tsqr_tree_kernel<TC_>;
@@ -946,6 +1001,27 @@ void run_factor(Ctx& ctx, Tsqr& f) {
   };
   const int G = f.wl ? f.wplan.G : f.plan.G;
   f.Rlocal = f.nloc > 0 ? run_tree(f.Rleaf, G, f.nloc, f.locY, f.locT, f.locR) : f.Rleaf;
+  if (deferred_T && f.plan.total_tiles() > 0) {
+    // per-tile T factors on the aux stream, after the local tree: they run
+    // beside what follows it -- the one-CTA SVD of the truncation sweep, the
+    // R-fold of the orthonormalization sweep -- not beside the tree, whose
+    // nodes need a whole SM's shared memory each and were placed late when
+    // the T blocks got there first (tree 150 -> 176 us)
+    TTB_CUDA(cudaEventCreateWithFlags(&leaf_done, cudaEventDisableTiming));
+    TTB_CUDA(cudaEventRecord(leaf_done, st));
+    cudaStream_t ax = ctx.aux_stream();
+    TTB_CUDA(cudaStreamWaitEvent(ax, leaf_done, 0));
+    TTB_CUDA(cudaEventDestroy(leaf_done));
+    {
+      ProfScope pt("tile_T", ax);
+      smem_attr((const void*)tile_T_kernel, sizeof(TSmem));
+      tile_T_kernel<<<(unsigned)f.plan.total_tiles(), 256, sizeof(TSmem), ax>>>(f.T, f.b,
+                                                                                ((int64_t)f.b * f.b + 1) & ~1LL);
+      TTB_LAUNCHED();
+    }
+    TTB_CUDA(cudaEventCreateWithFlags(&f.t_ready, cudaEventDisableTiming));
+    TTB_CUDA(cudaEventRecord(f.t_ready, ax));
+  }
   if (ctx.nranks > 1) {
     // allgather the rank roots, then a redundant (bitwise identical) tree
     ctx.allgather(f.Rlocal, f.Rstack, (size_t)f.b * f.b);
@@ -1171,6 +1247,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
     ctx.free(scr);
     return;
   }
+  if (f.t_ready) TTB_CUDA(cudaStreamWaitEvent(ctx.stream, f.t_ready, 0));
   ChainArgs ca;
   ca.plan = f.plan;
   ca.ldy = f.ldy;
@@ -1213,6 +1290,11 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
 }
 
 void tsqr_release(Ctx& ctx, Tsqr& f) {
+  if (f.t_ready) {  // the aux stream may still be writing T into mem
+    TTB_CUDA(cudaStreamWaitEvent(ctx.stream, f.t_ready, 0));
+    TTB_CUDA(cudaEventDestroy(f.t_ready));
+    f.t_ready = nullptr;
+  }
   if (f.mem) ctx.free(f.mem);
   f.mem = nullptr;
 }
