@@ -308,6 +308,24 @@ void Ctx::sendrecv(int npeers, const int* peers, const double* const* send, cons
 
 void Ctx::sync() { TTB_CUDA(cudaStreamSynchronize(stream)); }
 
+bool Ctx::stage_init() {
+  if (stage_buf[0]) return true;
+  for (int i = 0; i < kStageSlots; ++i) {
+    if (cudaHostAlloc(&stage_buf[i], kStageBytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&stage_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      for (int k = 0; k <= i; ++k) {
+        if (stage_buf[k]) cudaFreeHost(stage_buf[k]);
+        if (stage_ev[k]) cudaEventDestroy(stage_ev[k]);
+        stage_buf[k] = nullptr;
+        stage_ev[k] = nullptr;
+      }
+      return false;
+    }
+  }
+  return true;
+}
+
 cudaStream_t Ctx::aux_stream() {
   if (!aux) TTB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
   return aux;
@@ -433,6 +451,10 @@ int ttb_ctx_destroy(ttb_ctx* ctx) {
     if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
     if (ctx->c.copy) cudaStreamDestroy(ctx->c.copy);
     if (ctx->c.mapped_host) cudaFreeHost(ctx->c.mapped_host);
+    for (int i = 0; i < Ctx::kStageSlots; ++i) {
+      if (ctx->c.stage_buf[i]) cudaFreeHost(ctx->c.stage_buf[i]);
+      if (ctx->c.stage_ev[i]) cudaEventDestroy(ctx->c.stage_ev[i]);
+    }
     if (ctx->c.dflag) cudaFree(ctx->c.dflag);
     delete ctx;
   }

@@ -35,6 +35,13 @@ struct Ctx {
   cudaStream_t aux_stream();
   cudaStream_t copy = nullptr;  // host<->device transfers of the host API (lazily created)
   cudaStream_t copy_stream();
+  // page-locked staging ring of the host API (pageable user buffers are
+  // copied through it by a worker thread; lazily allocated, kept)
+  static constexpr int kStageSlots = 4;
+  static constexpr size_t kStageBytes = size_t(32) << 20;
+  void* stage_buf[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t stage_ev[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  bool stage_init();  // false: no page-locked memory to be had (callers fall back to plain pageable copies)
   // small device -> host reads (ranks, norms) go through mapped pinned
   // memory written by a kernel: they never queue behind bulk DMA copies
   // (e.g. the host API's output downloads on the copy engine)

@@ -1,3 +1,4 @@
+#include <atomic>
 #include <chrono>
 // Native drivers behind the C ABI (include/ttb.h): TT construction, Gram
 // sweeps, orthonormalization and the four rounding variants.  These replace
@@ -5,7 +6,11 @@
 // ops.py:71-155) with a host loop that only enqueues kernels on the context
 // stream; the single host sync per truncation step reads back the kept rank.
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "ops.cuh"
@@ -369,8 +374,12 @@ int ttb_norm_ortho(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* ran
 // the compute stream waits for core n only where the sweep first reads it;
 // every output core is copied back as soon as it is final (event on the
 // stream that finished it), so both transfers overlap the sweeps.  Host
-// buffers that are not page-locked are registered for the duration of the
-// call (cudaHostRegister) so the copies stay asynchronous.
+// pageable buffers go through the context's page-locked staging ring: a
+// worker thread copies 32 MB chunks user -> ring with several host threads
+// while the copy engine drains the previous chunks (and the mirror image for
+// outputs), so the call neither page-locks user memory (cudaHostRegister
+// costs ~0.25 ms per MB: 570 ms on cfg3) nor falls back to the driver's
+// synchronous pageable copies (290 ms).
 struct HostIO {
   Ctx& ctx;
   int N;
@@ -379,53 +388,180 @@ struct HostIO {
   std::vector<cudaEvent_t> in_ev;
   std::vector<char> waited;
   std::vector<cudaEvent_t> evs;
-  std::vector<void*> registered;
+  // staging worker
+  struct Job {
+    int kind;  // 0: host -> device, 1: device -> host
+    int n;
+    const char* src;
+    char* dst;
+    size_t bytes;
+    cudaEvent_t after;  // D2H: the producer's completion
+  };
+  std::deque<Job> jobs;
+  std::mutex mu;
+  std::condition_variable cv_job, cv_rec;
+  std::vector<char> recorded;  // in_ev[n] has been recorded (staged uploads: by the worker)
+  bool closing = false;
+  std::atomic<bool> failed{false};
+  std::thread worker;
+  int slot = 0;
+  bool staged_ok = false;
+
   HostIO(Ctx& c, int n, const double* const* in, double* const* out)
-      : ctx(c), N(n), hin(in), hout(out), in_ev(n, nullptr), waited(n, 0) {}
+      : ctx(c), N(n), hin(in), hout(out), in_ev(n, nullptr), waited(n, 0), recorded(n, 0) {}
   cudaStream_t cs() { return ctx.copy_stream(); }
-  void pin(const void* p, size_t bytes) {
-    if (!p || bytes == 0) return;
+  static bool device_visible(const void* p) {
     cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) == cudaSuccess && (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
-                                                          a.type == cudaMemoryTypeManaged))
-      return;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess &&
+        (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged))
+      return true;
     cudaGetLastError();
-    if (cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault) == cudaSuccess)
-      registered.push_back(const_cast<void*>(p));
-    else
-      cudaGetLastError();  // copies stay correct, just synchronous
+    return false;
+  }
+  static void par_memcpy(char* dst, const char* src, size_t bytes) {
+    constexpr int kThreads = 6;
+    const size_t part = ((bytes / kThreads) + 4095) & ~size_t(4095);
+    if (bytes < (size_t(4) << 20) || part == 0) {
+      memcpy(dst, src, bytes);
+      return;
+    }
+    std::thread th[kThreads - 1];
+    int nth = 0;
+    size_t off = part;
+    for (; nth < kThreads - 1 && off < bytes; ++nth, off += part) {
+      const size_t len = std::min(part, bytes - off);
+      th[nth] = std::thread([=] { memcpy(dst + off, src + off, len); });
+    }
+    memcpy(dst, src, std::min(part, bytes));
+    for (int i = 0; i < nth; ++i) th[i].join();
+  }
+  void run_job(const Job& j) {
+    const size_t CH = Ctx::kStageBytes;
+    if (j.kind == 0) {
+      for (size_t off = 0; off < j.bytes; off += CH) {
+        const size_t len = std::min(CH, j.bytes - off);
+        const int s = slot++ % Ctx::kStageSlots;
+        TTB_CUDA(cudaEventSynchronize(ctx.stage_ev[s]));  // the slot's previous transfer has drained
+        par_memcpy((char*)ctx.stage_buf[s], j.src + off, len);
+        TTB_CUDA(cudaMemcpyAsync(j.dst + off, ctx.stage_buf[s], len, cudaMemcpyHostToDevice, cs()));
+        TTB_CUDA(cudaEventRecord(ctx.stage_ev[s], cs()));
+      }
+      TTB_CUDA(cudaEventRecord(in_ev[j.n], cs()));
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        recorded[j.n] = 1;
+      }
+      cv_rec.notify_all();
+    } else {
+      TTB_CUDA(cudaStreamWaitEvent(cs(), j.after, 0));
+      int prev = -1;
+      size_t poff = 0, plen = 0;
+      for (size_t off = 0; off < j.bytes; off += CH) {
+        const size_t len = std::min(CH, j.bytes - off);
+        const int s = slot++ % Ctx::kStageSlots;
+        TTB_CUDA(cudaEventSynchronize(ctx.stage_ev[s]));
+        TTB_CUDA(cudaMemcpyAsync(ctx.stage_buf[s], j.src + off, len, cudaMemcpyDeviceToHost, cs()));
+        TTB_CUDA(cudaEventRecord(ctx.stage_ev[s], cs()));
+        if (prev >= 0) {  // the previous chunk leaves the ring while this one arrives
+          TTB_CUDA(cudaEventSynchronize(ctx.stage_ev[prev]));
+          par_memcpy(j.dst + poff, (const char*)ctx.stage_buf[prev], plen);
+        }
+        prev = s;
+        poff = off;
+        plen = len;
+      }
+      if (prev >= 0) {
+        TTB_CUDA(cudaEventSynchronize(ctx.stage_ev[prev]));
+        par_memcpy(j.dst + poff, (const char*)ctx.stage_buf[prev], plen);
+      }
+    }
+  }
+  void worker_main() {
+    cudaSetDevice(ctx.device);
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_job.wait(lk, [&] { return closing || !jobs.empty(); });
+        if (jobs.empty()) return;
+        j = jobs.front();
+        jobs.pop_front();
+      }
+      try {
+        if (!failed) run_job(j);
+      } catch (...) {
+        failed = true;
+      }
+      if (failed && j.kind == 0) {  // never leave the compute thread waiting
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          recorded[j.n] = 1;
+        }
+        cv_rec.notify_all();
+      }
+    }
+  }
+  void submit(const Job& j) {
+    if (!worker.joinable()) worker = std::thread([this] { worker_main(); });
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      jobs.push_back(j);
+    }
+    cv_job.notify_one();
+  }
+  bool staged(const void* p, size_t bytes) {
+    static const bool off = getenv("TTB_HOSTIO_NOSTAGE") != nullptr;  // diagnostics: plain pageable copies
+    if (off || !p || bytes == 0 || device_visible(p)) return false;
+    if (!staged_ok) staged_ok = ctx.stage_init();
+    return staged_ok;
   }
   void upload(int n, double* dst, int64_t count) {
-    pin(hin[n], (size_t)count * sizeof(double));
-    pin(hout[n], (size_t)count * sizeof(double));
-    TTB_CUDA(cudaMemcpyAsync(dst, hin[n], (size_t)count * sizeof(double), cudaMemcpyHostToDevice, cs()));
+    const size_t bytes = (size_t)count * sizeof(double);
     TTB_CUDA(cudaEventCreateWithFlags(&in_ev[n], cudaEventDisableTiming));
+    if (staged(hin[n], bytes)) {
+      submit(Job{0, n, (const char*)hin[n], (char*)dst, bytes, nullptr});
+      return;
+    }
+    TTB_CUDA(cudaMemcpyAsync(dst, hin[n], bytes, cudaMemcpyHostToDevice, cs()));
     TTB_CUDA(cudaEventRecord(in_ev[n], cs()));
+    recorded[n] = 1;
   }
   void need(int n, cudaStream_t st) {
     if (n < 0 || n >= N || waited[n]) return;
+    if (!recorded[n]) {  // a staged upload: wait until the worker has enqueued its last chunk
+      std::unique_lock<std::mutex> lk(mu);
+      cv_rec.wait(lk, [&] { return recorded[n] != 0; });
+    }
+    TTB_CHECK(!failed, TTB_ERR_CUDA, "host staging copy failed");
     TTB_CUDA(cudaStreamWaitEvent(st, in_ev[n], 0));
     waited[n] = 1;
   }
-  struct Late { int n; const double* src; int64_t count; };
-  std::vector<Late> late;
   void ready(int n, const double* src, int64_t count, cudaStream_t st) {
     cudaEvent_t e;
     TTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     TTB_CUDA(cudaEventRecord(e, st));
-    TTB_CUDA(cudaStreamWaitEvent(cs(), e, 0));
     evs.push_back(e);
-    static const bool late_d2h = getenv("TTB_HOSTIO_LATE_D2H") != nullptr;  // diagnostics
-    if (late_d2h) {
-      late.push_back({n, src, count});
+    const size_t bytes = (size_t)count * sizeof(double);
+    if (staged(hout[n], bytes)) {
+      submit(Job{1, n, (const char*)src, (char*)hout[n], bytes, e});
       return;
     }
-    TTB_CUDA(cudaMemcpyAsync(hout[n], src, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, cs()));
+    if (worker.joinable()) drain();  // keep the copy stream's order: staged jobs first
+    TTB_CUDA(cudaStreamWaitEvent(cs(), e, 0));
+    TTB_CUDA(cudaMemcpyAsync(hout[n], src, bytes, cudaMemcpyDeviceToHost, cs()));
+  }
+  void drain() {
+    if (!worker.joinable()) return;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      closing = true;
+    }
+    cv_job.notify_all();
+    worker.join();
+    closing = false;
   }
   void finish() {
-    for (auto& l : late)
-      cudaMemcpyAsync(hout[l.n], l.src, (size_t)l.count * sizeof(double), cudaMemcpyDeviceToHost, cs());
-    late.clear();
+    drain();
     // the compute stream must not run past the copies (device buffers are
     // freed stream-ordered on it), and the caller reads host memory
     cudaEvent_t e;
@@ -438,10 +574,18 @@ struct HostIO {
     for (auto e2 : in_ev)
       if (e2) cudaEventDestroy(e2);
     for (auto e2 : evs) cudaEventDestroy(e2);
-    for (void* p : registered) cudaHostUnregister(p);
     in_ev.clear();
     evs.clear();
-    registered.clear();
+  }
+  ~HostIO() {
+    if (worker.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        closing = true;
+      }
+      cv_job.notify_all();
+      worker.join();
+    }
   }
 };
 
@@ -807,6 +951,7 @@ int ttb_round_host(ttb_ctx* h, int variant, double eps0, int64_t max_rank, int n
   io.finish();
   mark("copies done");
   ctx.free(dmem);
+  TTB_CHECK(!io.failed, TTB_ERR_CUDA, "host staging copy failed");
   TTB_TRY_END
 }
 

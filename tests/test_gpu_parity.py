@@ -304,6 +304,18 @@ def test_round_host_pinned_cfg1():
     assert meta["norm"] == pytest.approx(meta_ref["norm"], rel=TOL_SCALAR)
 
 
+def test_round_host_pageable_multichunk():
+    """Pageable numpy cores larger than the 32 MB staging chunk (several ring
+    slots per core, in and out): bitwise the device path's result."""
+    y = O.random_cores((60, 9000, 50), (1, 24, 24, 1), 7)
+    x = O.add(y, y)  # middle core 48 x 9000 x 48 doubles = 166 MB: six chunks
+    opts = T.RoundingOptions(1e-9, "LRLI")
+    dev_out = T.round_tt(dev(x), opts)
+    cores, meta = T.round_tt_host(x, opts)
+    assert meta["output_ranks"] == dev_out.ranks == (1, 24, 24, 1)
+    bitwise(cores, host(dev_out))
+
+
 def test_round_host_zero_and_single_mode():
     x = [np.zeros_like(c) for c in O.random_cores((4, 5, 4), (1, 3, 3, 1), 2)]
     cores, meta = T.round_tt_host(x, T.RoundingOptions(1e-6, "RLR"))
