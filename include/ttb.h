@@ -195,8 +195,10 @@ int ttb_round_hadamard(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank,
  * input ranks, results packed at the front as in ttb_round).  The upload of
  * core n overlaps the orthonormalization sweep up to core n, and each
  * output core is downloaded as soon as it is final.  Page-locked buffers
- * (cudaHostAlloc / torch pin_memory) give full PCIe bandwidth; others are
- * registered for the duration of the call.  Returns when out[] is filled. */
+ * (cudaHostAlloc / torch pin_memory) are copied directly at full PCIe
+ * bandwidth; pageable ones pass through the context's page-locked staging
+ * ring (a worker thread, 32 MB chunks), never registered.  Returns when
+ * out[] is filled. */
 int ttb_round_host(ttb_ctx* ctx, int variant, double eps0, int64_t max_rank, int ndim,
                    const int64_t* dims, const int64_t* ranks, const double* const* in,
                    double* const* out, int64_t* out_ranks, double* meta);

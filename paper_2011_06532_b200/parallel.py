@@ -240,7 +240,8 @@ def round_tt_host(cores, opts: RoundingOptions, comm=None, out=None):
     orthonormalization sweep and each output core is downloaded as soon as
     it is final (ttb_round_host).  ``out`` optionally supplies the output
     buffers (flat host arrays / tensors of at least r_left*I*r_right input
-    entries each; page-locked ones avoid per-call registration).
+    entries each; page-locked ones are copied directly, pageable ones
+    through the library's page-locked staging ring).
 
     Returns (cores, meta): F-order views into the output buffers, and the
     reference's meta dict (norm, eps_bond, output_ranks, ...)."""

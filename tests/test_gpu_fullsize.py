@@ -171,8 +171,11 @@ def test_cfg4_vs_oracle():
 
 def test_cfg5_vs_oracle():
     """Reported, not gated on 1e-10: both
-    sides' truncation errors and their difference; ranks must agree."""
-    n = 50_000 if avail_gb() >= 100 else 5000
+    sides' truncation errors and their difference; ranks must agree.  The
+    oracle needs ~10 minutes at the full n = 50000 (its result is recorded in
+    profiles/r2_fullsize_parity.txt), so the default run uses the survey's
+    n = 5000 and TTB_FULLSIZE=1 selects the full size."""
+    n = 50_000 if (os.environ.get("TTB_FULLSIZE") and avail_gb() >= 100) else 5000
     dims, r = (n,) * 12, (1,) + (8,) * 11 + (1,)
     x, w = dev_random(dims, r, 0), dev_random(dims, r, 1)
     p = T.hadamard(x, w)
