@@ -43,5 +43,13 @@ for w in range(nw):
 for j in range(5, 12):
     w = (j + 1) % nw
     s = c[w, j]
+    q = c[w, j + 1]  # publish_slot stamps its phases at the published column's index
     print(f"j={j} producer w{w}: top->full {s[1]-s[0]:.0f} full->fulls {s[2]-s[1]:.0f} fulls->pub3 {s[3]-s[2]:.0f} "
-          f"| rawpub(4) {s[4]-s[2]:.0f} sigma(5) {s[5]-s[4]:.0f} scalars(6) {s[6]-s[5]:.0f} pubsc(7) {s[7]-s[6]:.0f}")
+          f"| fulls->rawpub(4) {q[4]-s[2]:.0f} sigma(5) {q[5]-q[4]:.0f} scalars(6) {q[6]-q[5]:.0f} pubsc(7) {q[7]-q[6]:.0f} "
+          f"scale-own {s[3]-q[7]:.0f}")
+# chain: consecutive scalar publications and raw publications
+ws = [(j + 1) % nw for j in range(b - 1)]
+raw = np.array([c[ws[j], j + 1, 4] for j in range(4, b - 2)])
+sc = np.array([c[ws[j], j + 1, 7] for j in range(4, b - 2)])
+print("raw-publication period median %.0f, scalar-publication period median %.0f, raw->scalars median %.0f" % (
+    np.median(np.diff(raw)), np.median(np.diff(sc)), np.median(sc - raw)))
