@@ -1308,6 +1308,6 @@ extern "C" int ttb_dbg_tile(long long* out) {
 #endif
 #ifdef TTB_DEBUG_CLK
 extern "C" int ttb_dbg_clk(long long* out) {
-  return cudaMemcpyFromSymbol(out, ttb::g_dclk, sizeof(long long) * 8 * 64 * 8) == cudaSuccess ? 0 : 5;
+  return cudaMemcpyFromSymbol(out, ttb::g_dclk, sizeof(long long) * 16 * 64 * 16) == cudaSuccess ? 0 : 5;
 }
 #endif

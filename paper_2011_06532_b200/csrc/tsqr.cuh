@@ -259,16 +259,16 @@ constexpr int kRing = 4;  // Householder vectors in flight between warps
 // Debug-only cycle stamps of the column pipeline (CTA 0, second tile):
 // build with NVCC_EXTRA=-DTTB_DEBUG_CLK, read back with ttb_dbg_clk.
 #ifdef TTB_DEBUG_CLK
-static __device__ long long g_dclk[16 * 64 * 8];
+static __device__ long long g_dclk[16 * 64 * 16];
 #define TTB_DCLK(ph)                                                                     \
   do {                                                                                   \
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && gbase == b && j < 64 && threadIdx.x < 512) \
-      g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                      \
+      g_dclk[((threadIdx.x >> 5) * 64 + j) * 16 + (ph)] = clock64();                     \
   } while (0)
 #define TTB_DCLK2(ph)                                                                        \
   do {                                                                                       \
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (gj - j) > 0 && (gj - j) <= 64 && j < 64 && threadIdx.x < 512) \
-      g_dclk[((threadIdx.x >> 5) * 64 + j) * 8 + (ph)] = clock64();                          \
+      g_dclk[((threadIdx.x >> 5) * 64 + j) * 16 + (ph)] = clock64();                         \
   } while (0)
 #else
 #define TTB_DCLK(ph) \
@@ -482,7 +482,9 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
       *reinterpret_cast<double2*>(&xb[C::row(s, lr)]) = make_double2(x0, x1);
     }
   }
+  TTB_DCLK2(10);
   __syncwarp();
+  TTB_DCLK2(11);
   if (lane == 0) mbar_arrive(&sm.full[slot]);
   TTB_DCLK2(4);
   // 2. scalars
@@ -512,7 +514,9 @@ __device__ __forceinline__ void publish_slot(double (&A)[C::RPL][C::CPL], int j,
     double2* scp = reinterpret_cast<double2*>(sm.sc[slot]);
     scp[0] = make_double2(tau, scal);
     scp[1] = make_double2(bv, beta);
+    TTB_DCLK2(12);
     mbar_arrive(&sm.fulls[slot]);
+    TTB_DCLK2(13);
     sm.taus[j] = tau;  // off the chain: read at the end of the tile
     if (!HEAD) sm.Rs[j + BM * j] = beta;
   }
@@ -679,6 +683,7 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
       c[t] = tau * d[t] * scal;
     }
     const int tn = producer ? C::owner_slot(nx) : -1;
+    TTB_DCLK(8);
 #define TTB_UPD(T) update_slot<C, HEAD, T>(A, xr, c[T], beta, tau * d[T], kk[T], j, b, lr, sm)
     if (producer) {  // the next column first: it is on the critical path
       switch (tn) {
@@ -691,6 +696,7 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
         case 6: TTB_UPD((kSlot<C, 6>)); break;
         default: TTB_UPD((kSlot<C, 7>)); break;
       }
+      TTB_DCLK(9);
       publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
     }

@@ -25,11 +25,11 @@ for _ in range(3):
                                    C.c_void_p(R.data_ptr())))
     torch.cuda.synchronize()
     lib.ttb_tsqr_free(comm.ctx(), h)
-buf = np.zeros(16 * 64 * 8, dtype=np.int64)
+buf = np.zeros(16 * 64 * 16, dtype=np.int64)
 f = lib.ttb_dbg_clk
 f.argtypes = [C.c_void_p]
 assert f(buf.ctypes.data) == 0
-c = buf.reshape(16, 64, 8).astype(np.float64)  # [warp][j][phase]
+c = buf.reshape(16, 64, 16).astype(np.float64)  # [warp][j][phase]
 nw = max(w for w in range(16) if c[w, 1, 0] > 0) + 1
 base = c[0, 0, 0]
 print("warps", nw, "b", b)
@@ -47,6 +47,8 @@ for j in range(5, 12):
     print(f"j={j} producer w{w}: top->full {s[1]-s[0]:.0f} full->fulls {s[2]-s[1]:.0f} fulls->pub3 {s[3]-s[2]:.0f} "
           f"| fulls->rawpub(4) {q[4]-s[2]:.0f} sigma(5) {q[5]-q[4]:.0f} scalars(6) {q[6]-q[5]:.0f} pubsc(7) {q[7]-q[6]:.0f} "
           f"scale-own {s[3]-q[7]:.0f}")
+    print(f"      fulls->d,c {s[8]-s[2]:.0f}  update {s[9]-s[8]:.0f}  dispatch+stores {q[10]-s[9]:.0f}  syncwarp {q[11]-q[10]:.0f}  "
+          f"arrive(full) {q[4]-q[11]:.0f} | sc stores {q[12]-q[6]:.0f}  arrive(fulls) {q[13]-q[12]:.0f}  taus/R stores {q[7]-q[13]:.0f}")
 # chain: consecutive scalar publications and raw publications
 ws = [(j + 1) % nw for j in range(b - 1)]
 raw = np.array([c[ws[j], j + 1, 4] for j in range(4, b - 2)])
