@@ -556,7 +556,9 @@ __device__ __forceinline__ void publish(double (&A)[C::RPL][C::CPL], int j, int 
 }
 
 // finish column slot T for reflector j: a -= c x (+ head pivot-row fix)
-template <class C, bool HEAD, int T>
+// RW: also update the chain triangle's entry R[j, k] (the producer's slot does
+// that after the next column is published: it is off the column chain)
+template <class C, bool HEAD, int T, bool RW = true>
 __device__ __forceinline__ void update_slot(double (&A)[C::RPL][C::CPL], const double (&xr)[C::RPL], double c,
                                             double beta, double rcoef, int k, int j, int b, int lr, TileSmem<C>& sm) {
   if (k > j && k < b) {
@@ -566,7 +568,7 @@ __device__ __forceinline__ void update_slot(double (&A)[C::RPL][C::CPL], const d
       if (HEAD && C::pivot_slot(s) && C::row(s, lr) == j) a = fma(c, beta, a);
       A[s][T] = a;
     }
-    if (!HEAD && lr == 0) sm.Rs[j + C::BMAX * k] -= rcoef;
+    if (RW && !HEAD && lr == 0) sm.Rs[j + C::BMAX * k] -= rcoef;
   }
 }
 
@@ -685,21 +687,30 @@ __device__ void tile_qr_t(double (&A)[C::RPL][C::CPL], int b, TileSmem<C>& sm, i
     const int tn = producer ? C::owner_slot(nx) : -1;
     TTB_DCLK(8);
 #define TTB_UPD(T) update_slot<C, HEAD, T>(A, xr, c[T], beta, tau * d[T], kk[T], j, b, lr, sm)
-    if (producer) {  // the next column first: it is on the critical path
+    // the next column first (it is on the critical path): its update and its
+    // publication in ONE dispatch on the owner slot (column nx > j always
+    // needs the update), the R entry afterwards
+#define TTB_UPDPUB(T)                                                                                    \
+  do {                                                                                                   \
+    update_slot<C, HEAD, T, false>(A, xr, c[T], beta, tau * d[T], kk[T], j, b, lr, sm);                  \
+    TTB_DCLK(9);                                                                                         \
+    publish_slot<C, HEAD, T>(A, nx, gj + 1, sm);                                                         \
+    if (!HEAD && lr == 0 && kk[T] > j && kk[T] < b) sm.Rs[j + BM * kk[T]] -= tau * d[T];                 \
+  } while (0)
+    if (producer) {
       switch (tn) {
-        case 0: TTB_UPD(0); break;
-        case 1: TTB_UPD(T1); break;
-        case 2: TTB_UPD((kSlot<C, 2>)); break;
-        case 3: TTB_UPD((kSlot<C, 3>)); break;
-        case 4: TTB_UPD((kSlot<C, 4>)); break;
-        case 5: TTB_UPD((kSlot<C, 5>)); break;
-        case 6: TTB_UPD((kSlot<C, 6>)); break;
-        default: TTB_UPD((kSlot<C, 7>)); break;
+        case 0: TTB_UPDPUB(0); break;
+        case 1: TTB_UPDPUB(T1); break;
+        case 2: TTB_UPDPUB((kSlot<C, 2>)); break;
+        case 3: TTB_UPDPUB((kSlot<C, 3>)); break;
+        case 4: TTB_UPDPUB((kSlot<C, 4>)); break;
+        case 5: TTB_UPDPUB((kSlot<C, 5>)); break;
+        case 6: TTB_UPDPUB((kSlot<C, 6>)); break;
+        default: TTB_UPDPUB((kSlot<C, 7>)); break;
       }
-      TTB_DCLK(9);
-      publish<C, HEAD>(A, nx, gj + 1, sm);
       TTB_DCLK(3);
     }
+#undef TTB_UPDPUB
     __syncwarp();  // slot gj consumed by every lane of this warp (x and scalars are in registers)
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
 #ifndef TTB_EXPT_NOUPD  // timing experiment only: skip the off-critical-path updates
