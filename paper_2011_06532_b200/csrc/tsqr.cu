@@ -809,42 +809,47 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
   const int ldu = ldpad(k);
   const int halves = ldy / UR;
   const int64_t nunits = pl.total_tiles() * halves;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);  // stage full (tx bytes)
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem_raw + 64);                  // warps done with a stage
   double* Ysb = reinterpret_cast<double*>(smem_raw + 128);
   const int64_t ystage = ustride * upw, ustage = (int64_t)b * ldu;
   const int S = a.stages;
   double* Usb = Ysb + S * ystage;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(Usb + S * ustage);  // UR entries
   const unsigned ubytes = (unsigned)(ustage * 8);
   if (threadIdx.x == 0) {
-    for (int s2 = 0; s2 < S; ++s2) mbar_init(&bar[s2], 1);
+    for (int s2 = 0; s2 < S; ++s2) {
+      mbar_init(&bar[s2], 1);
+      cnt[s2] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // warp 0 issues the copies of one unit into a stage
+  // one thread issues the copies of a work unit into a stage (the unit is one
+  // contiguous block: unit-major Y layout)
   auto issue = [&](int64_t unit, int st) {
-    if (threadIdx.x >= 32) return;
     const int64_t tile = unit / halves;
     const int r0 = (int)(unit - tile * halves) * UR;
-    if (threadIdx.x == 0) mbar_expect_tx(&bar[st], (unsigned)(ystage * 8) + ubytes);
-    __syncwarp();
-    // the unit is one contiguous block (unit-major Y layout)
     const double* Yg = a.Y + tile * y_tile_stride(ldy, b) + (int64_t)(r0 / kYUnit) * b * kYLd;
-    if (threadIdx.x == 0) {
-      bulk_g2s(Ysb + st * ystage, Yg, (unsigned)(ystage * 8), &bar[st]);
-      bulk_g2s(Usb + st * ustage, a.u + tile * ustage, ubytes, &bar[st]);
-    }
+    mbar_expect_tx(&bar[st], (unsigned)(ystage * 8) + ubytes);
+    bulk_g2s(Ysb + st * ystage, Yg, (unsigned)(ystage * 8), &bar[st]);
+    bulk_g2s(Usb + st * ustage, a.u + tile * ustage, ubytes, &bar[st]);
   };
   int64_t unit = blockIdx.x;
-  for (int s2 = 0; s2 < S - 1; ++s2)  // S - 1 units in flight ahead of the one being multiplied
-    if (unit + (int64_t)s2 * gridDim.x < nunits) issue(unit + (int64_t)s2 * gridDim.x, s2);
+  if (threadIdx.x == 0)
+    for (int s2 = 0; s2 < S; ++s2)
+      if (unit + (int64_t)s2 * gridDim.x < nunits) issue(unit + (int64_t)s2 * gridDim.x, s2);
+  // No CTA-wide barrier per unit: every warp waits for the stage, computes its
+  // output tiles with row offsets it derives itself, and counts itself out of
+  // the stage; the LAST warp out refills the stage with the unit S ahead.
+  // Warps drift apart by up to a unit, so the output stores of one overlap the
+  // MMAs of the others (in lockstep every warp reached its MMA phase together:
+  // math_pipe_throttle was the first stall reason with the pipe 49 % busy).
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const int64_t cstride = a.out.trans ? 1 : a.out.rl * a.out.I;
+  double* ob = a.out.base;
   for (int it = 0; unit < nunits; ++it, unit += gridDim.x) {
     const int st = it % S;
-    const int64_t nxt = unit + (int64_t)(S - 1) * gridDim.x;
-    if (nxt < nunits) {  // its stage was released by the barrier that ended the previous unit
-      if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(nxt, (it + S - 1) % S);
-    }
     const int64_t tile = unit / halves;
     const int r0 = (int)(unit - tile * halves) * UR;
     int g;
@@ -858,31 +863,27 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
     const double* z0 = a.z0 + (int64_t)g * b * k;
     const double* Ys = Ysb + st * ystage;
     const double* Us = Usb + st * ustage;
-    // output address of unit row m: rowoff[m] + n * cstride (one division per
-    // row here instead of one per element in the epilogue)
-    const int64_t cstride = a.out.trans ? 1 : a.out.rl * a.out.I;
-    for (int m = threadIdx.x; m < rows; m += kProdNT) {
-      int si, w;
-      tile_row(a.out.trans, r0 + m, nsl, rs, si, w);
-      rowoff[m] = a.out.addr(w, ia + si, 0);
-    }
     mbar_wait(&bar[st], (it / S) & 1);
-    __syncthreads();
     if (rows > 0) {
-      double* ob = a.out.base;
       // 16 x 8 output tiles on the m16n8k8 fp64 MMA; Y rows beyond `rows`
       // are exact zeros (zero-padded leaf tiles), so only the reflector index
       // needs a bound (columns of u beyond k only feed outputs never stored)
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      const int gq = lane >> 2, t4 = lane & 3;
       const int mt = (rows + 15) >> 4, ntl = (k + 7) >> 3, kst = (b + 7) >> 3;
       // two output tiles per warp pass share a row tile (the A fragments) and
-      // run as two independent MMA chains (one dependent chain per warp left
-      // the fp64 tensor pipe ~60 % idle)
+      // run as two independent MMA chains
       const int ntiles2 = mt * ((ntl + 1) >> 1);
       for (int tt = warp; tt < ntiles2; tt += NW) {
         const int m0 = (tt % mt) * 16, n0 = (tt / mt) * 16;
         const bool two = n0 + 8 < k;
+        // output addresses of this lane's two rows (one division pair per row)
+        int64_t ro[2];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int m = m0 + gq + 8 * h2;
+          int si, w;
+          tile_row(a.out.trans, r0 + (m < rows ? m : 0), nsl, rs, si, w);
+          ro[h2] = a.out.addr(w, ia + si, 0);
+        }
         const double* ya = Ys + (m0 >> 7) * ustride + (m0 & (kYUnit - 1)) + gq;
         const double* ub = Us + n0 + gq;
         double d[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
@@ -901,15 +902,29 @@ __global__ void __launch_bounds__(kProdNT, 1) tsqr_product_kernel(ProductArgs a)
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int m = m0 + gq + 8 * ((i >> 1) & 1), n = n0 + 8 * (i >> 2) + 2 * t4 + (i & 1);
+          const int h2 = (i >> 1) & 1;
+          const int m = m0 + gq + 8 * h2, n = n0 + 8 * (i >> 2) + 2 * t4 + (i & 1);
           if (m < rows && n < k) {
             const double base = (head && m < b) ? z0[m + b * n] : 0.0;
-            ob[rowoff[m] + cstride * n] = base - (i < 4 ? d[i & 3] : e[i & 3]);
+            ob[ro[h2] + cstride * n] = base - (i < 4 ? d[i & 3] : e[i & 3]);
           }
         }
       }
     }
-    __syncthreads();
+    // this warp is done with the stage (its fragment loads have been consumed)
+    __syncwarp();
+    if (lane == 0) {
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(&cnt[st])) : "memory");
+      if (old == NW - 1) {  // last warp out: refill
+        cnt[st] = 0;
+        const int64_t nxt = unit + (int64_t)S * gridDim.x;
+        if (nxt < nunits) {
+          fence_proxy_async();
+          issue(nxt, st);
+        }
+      }
+    }
   }
 }
 // ------------------------------------------------------------------------
@@ -1280,7 +1295,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.unit_rows = kYUnit * pa.upw;
   const size_t pstage = (size_t)pa.upw * ubytes1 + (size_t)b * ldpad(k) * sizeof(double);
   pa.stages = (int)std::max<size_t>(2, std::min<size_t>(kProdMaxStages, (200 * 1024) / pstage));
-  const size_t psmem = 128 + (size_t)pa.stages * pstage + (size_t)pa.unit_rows * sizeof(int64_t);
+  const size_t psmem = 128 + (size_t)pa.stages * pstage;
   ProfScope ps("apply_product", ctx.stream);
   const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);
   const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunits, ctx.num_sms));
