@@ -788,12 +788,16 @@ __device__ void store_Y_units(const double (&A)[C::RPL][C::CPL], int b, bool hea
   for (int t = 0; t < C::CPL; ++t) {
     const int k = col_of<C>(t, warp, lc);
     if (k >= b) continue;
+    // rows come in pairs (2 lr, 2 lr + 1): one 16-byte store per pair
 #pragma unroll
-    for (int s = 0; s < C::RPL; ++s) {
+    for (int s = 0; s < C::RPL; s += 2) {
       const int r = C::row(s, lr);
-      double v = A[s][t];
-      if (head) v = r < k ? 0.0 : (r == k ? 1.0 : v);
-      Y[y_index(r, k, b)] = v;
+      double v0 = A[s][t], v1 = A[s + 1][t];
+      if (head) {
+        v0 = r < k ? 0.0 : (r == k ? 1.0 : v0);
+        v1 = r + 1 < k ? 0.0 : (r + 1 == k ? 1.0 : v1);
+      }
+      *reinterpret_cast<double2*>(&Y[y_index(r, k, b)]) = make_double2(v0, v1);
     }
   }
 }
