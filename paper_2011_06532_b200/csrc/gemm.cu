@@ -156,12 +156,16 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) 
   const int ldS = ((K + 11) & ~15) + 4;  // >= K, 4 mod 16
   const int MP = (M + 15) & ~15, KP = (K + 3) & ~3;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(fsm);
+  unsigned* cnt = reinterpret_cast<unsigned*>(fsm + 8);  // warps done with a stage
   double* Ss = fsm + 16;                          // MP x ldS (row m)
   double* Bs = Ss + (int64_t)MP * ldS;            // stages of K x kFoldJ
   Bs += (16 - ((Bs - fsm) & 15)) & 15;
   constexpr int ldB = kFoldJ + 4;                 // RIGHT: row stride of a stage
   const int64_t bstage = RIGHT ? (int64_t)K * ldB : (int64_t)K * kFoldJ;
-  if (tid < kFoldStages) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fd_smem(&bar[tid])) : "memory");
+  if (tid < kFoldStages) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fd_smem(&bar[tid])) : "memory");
+    cnt[tid] = 0;
+  }
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   for (int idx = tid; idx < MP * ldS; idx += kFoldNT) {
     const int m = idx / ldS, k = idx % ldS;
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) 
     const int nj = (int)min64(kFoldJ, N - j0);
     const unsigned bytes = (unsigned)(K * nj * 8);
     if constexpr (!RIGHT) {
-      if (tid != 0) return;
+      if (lane != 0) return;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
                    : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -182,12 +186,11 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) 
                    "l"(a.B + K * j0), "r"(bytes), "r"(fd_smem(&bar[st]))
                    : "memory");
     } else {
-      if (tid >= 32) return;
-      if (tid == 0)
+      if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fd_smem(&bar[st])), "r"(bytes)
                      : "memory");
       __syncwarp();
-      for (int k = tid; k < K; k += 32)
+      for (int k = lane; k < K; k += 32)
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                          fd_smem(Bs + st * bstage + (int64_t)k * ldB)),
                      "l"(a.B + j0 + a.bsk * k), "r"((unsigned)(nj * 8)), "r"(fd_smem(&bar[st]))
@@ -195,7 +198,8 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) 
     }
   };
   int st = 0, ph = 0, fill = 0;
-  for (int64_t c = blockIdx.x; c < nch && fill < kFoldStages; c += gridDim.x, ++fill) issue(c, fill);
+  if (warp == 0)  // issue() is run by one whole warp
+    for (int64_t c = blockIdx.x; c < nch && fill < kFoldStages; c += gridDim.x, ++fill) issue(c, fill);
   const int mt = MP / 16, ntl = kFoldJ / 16;
   for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const int64_t j0 = c * kFoldJ;
@@ -249,11 +253,22 @@ __global__ void __launch_bounds__(kFoldNT, kFoldMinB) fold_kernel(SkinnyArgs a) 
             }
           }
     }
-    __syncthreads();  // stage st consumed
-    const int64_t nxt = c + (int64_t)kFoldStages * gridDim.x;
-    if (nxt < nch) {
-      if (tid == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(nxt, st);
+    // no CTA-wide barrier per chunk: every warp counts itself out of the stage
+    // and the last one out refills it, so the stores of one warp overlap the
+    // MMAs of the others
+    __syncwarp();
+    unsigned old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(fd_smem(&cnt[st])) : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == NW - 1) {
+      if (lane == 0) cnt[st] = 0;
+      const int64_t nxt = c + (int64_t)kFoldStages * gridDim.x;
+      if (nxt < nch) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        issue(nxt, st);
+      }
     }
     if (++st == kFoldStages) {
       st = 0;
