@@ -440,11 +440,25 @@ def measure_norms(T, comm, reps=5):
 # ---------------------------------------------------------------------------
 # reference arm: the CPU path alone
 # ---------------------------------------------------------------------------
+def _load_ttpar():
+    """The UNMODIFIED reference package staged under baseline/_ref (pip install
+    --target of /root/reference/pkg), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ttpar")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import ttpar  # noqa: F401
+        return ttpar
+    except Exception:
+        sys.path.remove(ref)
+        return None
+
+
 def run_reference(args):
     rank, world, local = env_rank()
     if rank != 0:
         return
-    from oracle import tt_oracle as O
     from paper_2011_06532_b200 import cost
 
     cfg = args.config
@@ -454,17 +468,34 @@ def run_reference(args):
     # cores, so the default --steps/--warmup run takes a few minutes
     n = dims[0]
     sdims = dims
+    ttpar = _load_ttpar()
     t0 = time.perf_counter()
-    y = O.random_cores(sdims, ry, 0)
-    t_gen = time.perf_counter() - t0
-    x = O.add(y, y)
+    if ttpar is not None:
+        # the reference's own public API and stock code path:
+        # round_tt(serial_tt(X), RoundingOptions(...)), parallel.py:293
+        y = ttpar.random_tt(sdims, ry, 0)
+        t_gen = time.perf_counter() - t0
+        x = ttpar.serial_tt(ttpar.add(y, y))
+        opts = ttpar.RoundingOptions(eps0, "LRLI", maxr)
+        step = lambda: ttpar.round_tt(x, opts)  # noqa: E731
+        ranks_of = lambda o: tuple(o.ranks)  # noqa: E731
+        kind, what = "reference", "ttpar.round_tt(serial_tt(X)) from baseline/_ref (the unmodified reference package"
+    else:
+        from oracle import tt_oracle as O
+
+        y = O.random_cores(sdims, ry, 0)
+        t_gen = time.perf_counter() - t0
+        x = O.add(y, y)
+        step = lambda: O.round_tt(x, eps0, "LRLI", maxr)[0]  # noqa: E731
+        ranks_of = O.ranks_of
+        kind, what = "port", "oracle.round_tt (the oracle port: baseline/_ref is absent"
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        out, meta = O.round_tt(x, eps0, "LRLI", maxr)
+        out = step()
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
-    assert O.ranks_of(out) == tuple(ry)
+    assert ranks_of(out) == tuple(ry)
     B = cost.rounding_bytes(sdims, rx, ry)
     t = float(np.mean(times))
     value = B / t / 1e9
@@ -486,9 +517,9 @@ def run_reference(args):
         "config": {"workload": f"{cfg}: round_tt(X = Y + Y) d={len(dims)} n={dims[0]} ranks {rx[1]}->{ry[1]}, "
                                f"tol {eps0}, LRLI", "dims": list(sdims), "in_ranks": list(rx),
                    "out_ranks": list(ry), "same_config": True},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": f"the full workload (n={n}, same X as our arm: random_tt seed 0, X = Y + Y), "
-                                   f"oracle.round_tt (numpy + scipy LAPACK/OpenBLAS, {threads} threads), "
+                                   f"{what}; numpy + scipy LAPACK/OpenBLAS, {threads} threads), "
                                    f"mean of {args.steps} steps; input generation {t_gen:.1f} s untimed",
                          "threadpools": threadpool_desc()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
