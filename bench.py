@@ -370,30 +370,40 @@ def threadpool_desc():
 
 
 def cpu_baseline_same_input(x, out, dims, rx, ry, eps0, maxr):
-    """The CPU restatement of the reference (oracle/) on the same X, all host
-    threads; one step (~6 s on 16 cores for cfg3).  Its result is also the
-    full-size parity check of the GPU output ``out`` (BASELINE.md section 4
-    step 7): ranks identical, TT-form relative difference by the ortho route,
-    and the norm."""
+    """The reference on the same X, all host threads; one step (~6 s on 16
+    cores for cfg3): the unmodified package staged under baseline/_ref
+    (ttpar.round_tt(serial_tt(X)), kind "reference") when present, else its
+    CPU restatement (oracle/, kind "port").  Its result is also the full-size
+    parity check of the GPU output ``out``:
+    ranks identical, TT-form relative difference by the ortho route (computed
+    with the oracle's error routine), and the norm."""
     from oracle import tt_oracle as O
 
     cores = [np.asfortranarray(s.detach().cpu().numpy()) for s in x.local]
     threads = os.cpu_count() or 1
+    ttpar = _load_ttpar()
     t0 = time.perf_counter()
-    ref, meta = O.round_tt(cores, eps0, "LRLI", maxr)
-    dt = time.perf_counter() - t0
+    if ttpar is not None:
+        ro = ttpar.round_tt(ttpar.serial_tt(ttpar.TTTensor(cores)), ttpar.RoundingOptions(eps0, "LRLI", maxr))
+        dt = time.perf_counter() - t0
+        ref, meta = [np.asfortranarray(c.array) for c in ttpar.gather(ro).cores], ro.meta
+        kind, what = "reference", "ttpar.round_tt(serial_tt(X)) from baseline/_ref (the unmodified reference package"
+    else:
+        ref, meta = O.round_tt(cores, eps0, "LRLI", maxr)
+        dt = time.perf_counter() - t0
+        kind, what = "port", "oracle.round_tt (the oracle port: baseline/_ref is absent"
     from paper_2011_06532_b200 import cost
 
     B = cost.rounding_bytes(dims, rx, ry)
     got = [np.asfortranarray(s.detach().cpu().numpy()) for s in out.local]
     rel = O.rel_diff(got, ref)
-    parity = {"ranks_equal": tuple(out.ranks) == O.ranks_of(ref), "rel_err_ortho": rel,
+    parity = {"against": kind, "ranks_equal": tuple(out.ranks) == O.ranks_of(ref), "rel_err_ortho": rel,
               "norm_rel": abs(out.meta["norm"] - meta["norm"]) / meta["norm"],
               "bar": "ranks identical, rel_err_ortho <= 1e-10, norm_rel <= 1e-12",
               "pass": bool(tuple(out.ranks) == O.ranks_of(ref) and rel <= 1e-10
                            and abs(out.meta["norm"] - meta["norm"]) <= 1e-12 * meta["norm"])}
-    cpu = {"value": B / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-           "sample": f"the full workload, 1 step ({dt:.1f} s): oracle.round_tt (numpy+scipy LAPACK/OpenBLAS, "
+    cpu = {"value": B / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+           "sample": f"the full workload, 1 step ({dt:.1f} s): {what}; numpy + scipy LAPACK/OpenBLAS, "
                      f"{threads} threads) on the same X copied to host",
            "threadpools": threadpool_desc()}
     return cpu, parity
