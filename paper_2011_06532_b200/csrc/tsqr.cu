@@ -1295,7 +1295,9 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
   pa.unit_rows = kYUnit * pa.upw;
   const size_t pstage = (size_t)pa.upw * ubytes1 + (size_t)b * ldpad(k) * sizeof(double);
   pa.stages = (int)std::max<size_t>(2, std::min<size_t>(kProdMaxStages, (200 * 1024) / pstage));
-  const size_t psmem = 128 + (size_t)pa.stages * pstage;
+  // + 256: the B fragments of the last n-tile read up to 7 columns past k in
+  // the last row of u (they only feed outputs that are never stored)
+  const size_t psmem = 128 + (size_t)pa.stages * pstage + 256;
   ProfScope ps("apply_product", ctx.stream);
   const int64_t nunits = ntiles * (f.ldy / pa.unit_rows);
   const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunits, ctx.num_sms));

@@ -316,6 +316,35 @@ def test_round_host_pageable_multichunk():
     bitwise(cores, host(dev_out))
 
 
+@pytest.mark.parametrize("variant", ["LRLI", "RLRI", "LRL", "RLR"])
+def test_round_rank40_to_20_short_end_cores(variant):
+    """Ranks 40 -> 20 with short end cores: single-chain panels whose apply
+    product has k = 20 columns in an ld-20 staging row (the last n-tile's B
+    fragments read past k in the last stage: a regression once faulted here)."""
+    y = O.random_cores((300, 4000, 200), (1, 20, 20, 1), 11)
+    x = O.add(y, y)
+    out = T.round_tt(dev(x), T.RoundingOptions(1e-9, variant))
+    ref, _ = O.round_tt(x, 1e-9, variant)
+    assert out.ranks == O.ranks_of(ref) == (1, 20, 20, 1)
+    assert O.rel_diff(host(out), ref) < TOL_TT
+
+
+def test_round_host_mixed_pinned_and_pageable():
+    """Pageable inputs with page-locked outputs and the reverse (the staged
+    and the direct copies share the copy stream): same results."""
+    y = O.random_cores((300, 4000, 200), (1, 20, 20, 1), 11)
+    x = O.add(y, y)  # middle core 40 x 4000 x 40 doubles = 51 MB: two staging chunks
+    opts = T.RoundingOptions(1e-9, "RLRI")
+    want = host(T.round_tt(dev(x), opts))
+    pinned_out = [torch.empty(c.size, dtype=torch.float64).pin_memory() for c in x]
+    cores, meta = T.round_tt_host(x, opts, out=pinned_out)  # pageable in, pinned out
+    bitwise([np.asfortranarray(c.numpy() if hasattr(c, "numpy") else c) for c in cores], want)
+    pinned_in = [torch.from_numpy(np.asfortranarray(c)).permute(2, 1, 0).contiguous().permute(2, 1, 0).pin_memory()
+                 for c in x]
+    cores, meta = T.round_tt_host(pinned_in, opts)  # pinned in, pageable out
+    bitwise([np.asfortranarray(c.numpy() if hasattr(c, "numpy") else c) for c in cores], want)
+
+
 def test_round_host_zero_and_single_mode():
     x = [np.zeros_like(c) for c in O.random_cores((4, 5, 4), (1, 3, 3, 1), 2)]
     cores, meta = T.round_tt_host(x, T.RoundingOptions(1e-6, "RLR"))
