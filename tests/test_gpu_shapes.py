@@ -1,0 +1,114 @@
+"""Seeded random shapes: the CUDA path against the CPU oracle on chains whose
+dimensions, ranks and structure vary widely -- mode sizes from 1 to a few
+thousand, bond ranks 1..64 across the three register-tile classes (16 / 32 /
+64 columns), short end cores (single-chain panels, ragged last tiles), rank-
+deficient sums, every rounding variant, tolerance and rank-cap truncation.
+The fixed cases of tests/test_gpu_parity.py follow the reference's own tests;
+this sweep is for the tile / unit / stage boundaries in between (an apply
+product with k = 20 columns once read past its staging buffer on exactly such
+a shape).  Reference paths: parallel.py:164-438, ops.py:44-235."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2011_06532_b200 as T  # noqa: E402
+from oracle import tt_oracle as O  # noqa: E402
+
+TOL_TT = 1e-10
+TOL_SCALAR = 1e-12
+VARIANTS = ("LRLI", "RLRI", "LRL", "RLR")
+
+
+def dev(cores):
+    return T.serial_tt(T.TTTensor(cores))
+
+
+def host(dt):
+    return [c.array for c in T.gather(dt).cores]
+
+
+def chain(seed):
+    """dims, ranks of a random chain (about <= 2e6 entries per core)."""
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.integers(2, 6))
+    rmax = int(rng.choice([3, 9, 16, 17, 24, 32]))  # doubled by X = Y + Z: up to 64
+    ranks = [1] + [int(rng.integers(1, rmax + 1)) for _ in range(d - 1)] + [1]
+    dims = []
+    for n in range(d):
+        kind = rng.integers(0, 4)
+        if kind == 0:
+            m = int(rng.integers(1, 8))            # tiny mode
+        elif kind == 1:
+            m = int(rng.integers(8, 300))
+        elif kind == 2:
+            m = int(rng.integers(300, 3000))
+        else:
+            m = int(rng.choice([255, 256, 257, 511, 512, 513, 1023, 1024, 1025]))  # tile-size neighbours
+        cap = max(1, 2_000_000 // (4 * ranks[n] * ranks[n + 1]))
+        dims.append(min(m, cap))
+    return tuple(dims), tuple(ranks)
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_chain_round_inner_norm(seed):
+    dims, ranks = chain(seed)
+    if seed % 5 == 4:  # a Hadamard product (ranks multiply: keep the factors <= 8)
+        ranks = tuple(min(r, 8) for r in ranks)
+    y = O.random_cores(dims, ranks, seed)
+    z = O.random_cores(dims, ranks, seed + 500)
+    if seed % 5 == 4:
+        x = O.hadamard(y, z)
+    else:
+        x = O.add(y, y) if seed % 3 == 0 else O.add(y, z)  # rank-deficient every third case
+    variant = VARIANTS[seed % 4]
+    dx = dev(x)
+    # scalars
+    ip_ref = O.inner(x, O.add(z, y))
+    ip = T.inner_product(dx, dev(O.add(z, y)))
+    assert abs(ip - ip_ref) <= TOL_SCALAR * max(abs(ip_ref), O.norm(x, "innerprod") * O.norm(O.add(z, y), "innerprod"))
+    nref = O.norm(x, "ortho")
+    for method in ("innerprod", "ortho"):
+        assert abs(T.norm(dx, method) - nref) <= 1e-9 * nref, (method, dims, ranks)
+    # rounding: tolerance, then a rank cap
+    eps = float(10.0 ** -(3 + seed % 8))
+    ref, _ = O.round_tt(x, eps, variant)
+    out = T.round_tt(dx, T.RoundingOptions(eps, variant))
+    assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant, eps)
+    assert O.rel_diff(host(out), ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, variant, eps)
+    # eps0 = 0 keeps every singular value that is not an exact zero, up to the
+    # cap.  On a bond whose rank is limited by a small mode (say 5 rows under a
+    # cap of 10) the surplus singular values are roundoff: LAPACK's gesdd
+    # returns them as tiny nonzeros, so the reference keeps them; the device
+    # Jacobi SVD deflates them to exact zeros and drops them (the same happens
+    # on the exactly dependent columns of X = Y + Y).  Ranks are therefore
+    # identical or smaller there, never larger, and the tensors agree.
+    cap = max(1, max(O.ranks_of(x)) // 3)
+    ref, _ = O.round_tt(x, 0.0, variant, cap)
+    out = T.round_tt(dx, T.RoundingOptions(0.0, variant, max_rank=cap))
+    got_r, ref_r = tuple(out.ranks), O.ranks_of(ref)
+    assert all(g <= r for g, r in zip(got_r, ref_r)), (dims, ranks, variant, cap, got_r, ref_r)
+    assert O.rel_diff(host(out), ref) < 1e-8, (dims, ranks, variant, cap)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_chain_orthonormalize(seed):
+    dims, ranks = chain(100 + seed)
+    x = O.add(O.random_cores(dims, ranks, seed), O.random_cores(dims, ranks, seed + 7))
+    for direction in ("left", "right"):
+        got = host(T.orthonormalize(dev(x), direction))
+        assert O.rel_diff(got, x) < TOL_TT, (dims, ranks, direction)
+        # the orthonormalized cores have orthonormal unfoldings (all but the last / first)
+        idx = range(len(got) - 1) if direction == "left" else range(1, len(got))
+        for n in idx:
+            c = got[n]
+            m = c.reshape(-1, c.shape[2], order="F") if direction == "left" else c.reshape(c.shape[0], -1, order="F").T
+            if m.shape[0] < m.shape[1]:
+                continue  # more columns than rows: no orthonormal columns to speak of
+            g = m.T @ m
+            # orthonormal columns (zero columns on rank-deficient bonds): a projector
+            assert np.abs(g @ g - g).max() < 1e-10, (dims, ranks, direction, n)
