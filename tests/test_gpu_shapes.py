@@ -112,3 +112,33 @@ def test_random_chain_orthonormalize(seed):
             g = m.T @ m
             # orthonormal columns (zero columns on rank-deficient bonds): a projector
             assert np.abs(g @ g - g).max() < 1e-10, (dims, ranks, direction, n)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_chain_multirank(seed):
+    """The same sweep through the native multi-rank path (in-process rank group,
+    tests/test_gpu_multirank.py): P = 2, 3 or 4 ranks, idle ranks allowed where a
+    mode has fewer slices than ranks; every rank keeps the same ranks, the result
+    matches the oracle and the serial device result's ranks."""
+    dims, ranks = chain(200 + seed)
+    P = 2 + seed % 3
+    y = O.random_cores(dims, ranks, seed)
+    z = O.random_cores(dims, ranks, seed + 31)
+    x = O.add(y, y) if seed % 2 == 0 else O.add(y, z)
+    variant = VARIANTS[seed % 4]
+    eps = float(10.0 ** -(4 + seed % 6))
+    ref, meta = O.round_tt(x, eps, variant)
+    tx = T.TTTensor(x)
+
+    def body(comm):
+        dx = T.distribute(tx, comm, allow_idle=True)
+        out = T.round_tt(dx, T.RoundingOptions(eps, variant))
+        return out.ranks, host(out), T.inner_product(dx, dx), T.norm(dx, "ortho")
+
+    res = T.run_local_ranks(P, body)
+    ip_ref = O.inner(x, x)
+    for rk, _, ip, nrm in res:
+        assert tuple(rk) == tuple(res[0][0]) == O.ranks_of(ref), (dims, ranks, P, variant, eps)
+        assert abs(ip - ip_ref) <= TOL_SCALAR * abs(ip_ref)
+        assert abs(nrm - meta["norm"]) <= 1e-9 * meta["norm"]
+    assert O.rel_diff(res[0][1], ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, P, variant, eps)
