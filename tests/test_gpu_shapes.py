@@ -142,3 +142,43 @@ def test_random_chain_multirank(seed):
         assert abs(ip - ip_ref) <= TOL_SCALAR * abs(ip_ref)
         assert abs(nrm - meta["norm"]) <= 1e-9 * meta["norm"]
     assert O.rel_diff(res[0][1], ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, P, variant, eps)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_chain_wide_ranks(seed):
+    """Bond ranks above 64 (the general path, csrc/wide.cu) on random chains:
+    sums of two chains with ranks up to 70 each, and mixed chains where only
+    some bonds are wide (narrow and wide kernels alternate within one sweep)."""
+    rng = np.random.default_rng(3000 + seed)
+    d = int(rng.integers(3, 5))
+    dims = tuple(int(rng.integers(90, 400)) for _ in range(d))
+    ranks = (1,) + tuple(int(rng.choice([5, 20, 33, 40, 70])) for _ in range(d - 1)) + (1,)
+    y = O.random_cores(dims, ranks, seed)
+    z = O.random_cores(dims, ranks, seed + 9)
+    x = O.add(y, y) if seed % 2 == 0 else O.add(y, z)
+    variant = VARIANTS[seed % 4]
+    dx = dev(x)
+    ip_ref = O.inner(x, x)
+    assert abs(T.inner_product(dx, dx) - ip_ref) <= TOL_SCALAR * abs(ip_ref)
+    eps = 1e-8
+    ref, meta = O.round_tt(x, eps, variant)
+    out = T.round_tt(dx, T.RoundingOptions(eps, variant))
+    assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant)
+    assert O.rel_diff(host(out), ref) < TOL_TT, (dims, ranks, variant)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_chain_round_hadamard(seed):
+    """Implicit Hadamard-then-round (ops.py:109-132 then parallel.py:293) on
+    random chains: ranks identical to rounding the materialised product by the
+    oracle, TT-form error within the bar."""
+    dims, ranks = chain(400 + seed)
+    ranks = tuple(min(r, 8) for r in ranks)
+    y = O.random_cores(dims, ranks, seed)
+    w = O.random_cores(dims, ranks, seed + 77)
+    variant = VARIANTS[seed % 4]
+    eps = float(10.0 ** -(4 + seed))
+    ref, _ = O.round_tt(O.hadamard(y, w), eps, variant)
+    out = T.round_hadamard(dev(y), dev(w), T.RoundingOptions(eps, variant))
+    assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant, eps)
+    assert O.rel_diff(host(out), ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, variant, eps)
