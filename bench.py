@@ -441,7 +441,10 @@ def measure_norms(T, comm, reps=5):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         ms = float(np.median(ts))
-        res[name] = {"value": nbytes / (ms * 1e-3) / 1e9, "ms": ms, "bytes": nbytes}
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        # the Gram sweep is HBM-bound: fraction of the measured copy bandwidth
+        res[name] = {"value": gbs, "ms": ms, "bytes": nbytes, "hbm_frac": gbs / hbm_peak()[0]}
+    res["hbm_peak_gbs"], res["hbm_peak_source"] = hbm_peak()
     del x, z
     torch.cuda.synchronize()
     return res
