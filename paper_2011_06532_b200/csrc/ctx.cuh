@@ -84,6 +84,7 @@ struct Tsqr {
   int b = 0, cls = 0;
   Panel panel;
   LeafPlan plan;
+  bool r_only = false;  // set by the caller before tsqr_factor: only R is wanted (no Y / T written, no apply)
   int wl = 0;    // 1: team-pipelined leaf (wleaf.cu): wplan, Y in 64-row tiles, T holds U = T^{-1}
   WPlan wplan;
   int ldy = 0, ldy_tree = 0, ftree = 0;

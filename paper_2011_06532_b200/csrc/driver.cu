@@ -356,6 +356,7 @@ int ttb_norm_ortho(ttb_ctx* h, int ndim, const int64_t* dims, const int64_t* ran
   for (int n = N - 1; n >= 1; --n) {
     const int b = (int)ranks[n];
     Tsqr f;
+    f.r_only = true;  // no implicit Q is ever applied: the leaf skips Y and T
     tsqr_factor(ctx, panel_of(work, ranks[n], dims[n], ranks[n + 1], 1), f);
     gemm_small_right(ctx, ranks[n - 1] * dims[n - 1], b, b, in[n - 1], f.R, b, true, buf[which], true);
     tsqr_release(ctx, f);

@@ -29,7 +29,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
 tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __restrict__ Tg,
-                 double* __restrict__ Rleaf, int defer_T) {
+                 double* __restrict__ Rleaf, int defer_T, int r_only) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem<C>& sm = *reinterpret_cast<TileSmem<C>*>(smem_raw);
   const int g = blockIdx.x;
@@ -129,11 +129,13 @@ tsqr_leaf_kernel(Panel P, LeafPlan plan, double* __restrict__ Yg, double* __rest
     tile_qr<C>(A, b, head, sm, t * b);
     TTB_TILE_CLK(t, 2);
     const int64_t tile = tb + t;
-    store_Y_units<C>(A, b, head, Yg + tile * y_tile_stride(C::MC, b));
+    if (!r_only) store_Y_units<C>(A, b, head, Yg + tile * y_tile_stride(C::MC, b));  // R-only: no Q to apply later
     if (head) extract_R<C>(A, b, sm);
     // the next tile's loads are in flight while T is formed
     if (t + 1 < ntiles) load_tile(t + 1);
-    if (defer_T) {
+    if (r_only) {
+      TTB_TILE_CLK(t, 5);
+    } else if (defer_T) {
       // T is formed outside the chain (tile_T_kernel, beside the tree): hand
       // over striu(V^T V) with tau on the diagonal
       TTB_TILE_CLK(t, 5);
@@ -972,9 +974,10 @@ void run_factor(Ctx& ctx, Tsqr& f) {
       // so the step stays at 20.5 ms: opt-in)
       static const bool dfr = getenv("TTB_LEAF_T") && std::string(getenv("TTB_LEAF_T")) == "defer";
       const int defer = dfr ? 1 : 0;
-      leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf, defer);
+      leaf<<<f.plan.G, LC_::NT, tile_smem<LC_>(), st>>>(f.panel, f.plan, f.Y, f.T, f.Rleaf, f.r_only ? 0 : defer,
+                                                         f.r_only ? 1 : 0);
       TTB_LAUNCHED();
-      deferred_T = defer != 0;
+      deferred_T = defer != 0 && !f.r_only;
     }
   }
   auto tree = tsqr_tree_kernel<TC_>;
@@ -1185,6 +1188,7 @@ void tsqr_apply(Ctx& ctx, const Tsqr& f, const double* z, int k, const Panel& ou
     wide_tsqr_apply(ctx, f, z, k, out);
     return;
   }
+  TTB_CHECK(!f.r_only, TTB_ERR_CONTRACT, "TSQR apply: the factor was computed for R only");
   TTB_CHECK(k >= 1 && k <= kApplyKM, TTB_ERR_CAPABILITY, "TSQR apply: k must be in [1, 64]");
   TTB_CHECK(out.rs() == f.panel.rs() && out.I == f.panel.I && out.ncols() == k, TTB_ERR_SHAPE,
             "TSQR apply: output view does not match the factored panel");
