@@ -95,6 +95,23 @@ static void side_join(Ctx& ctx, Ctx& sctx) {
   TTB_CUDA(cudaEventDestroy(e));
 }
 
+// diagnostics (TTB_DEBUG_NAN=1): count non-finite entries of a device array, synchronously
+static void dbg_nan(Ctx& ctx, cudaStream_t st, const char* what, int n, const double* p, int64_t count) {
+  static const bool on = getenv("TTB_DEBUG_NAN") != nullptr;
+  if (!on || !p || count <= 0) return;
+  std::vector<double> h((size_t)count);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost);
+  int64_t bad = 0;
+  double amax = 0.0;
+  for (double v : h) {
+    if (!std::isfinite(v)) ++bad;
+    else amax = std::max(amax, std::fabs(v));
+  }
+  fprintf(stderr, "[nan] %-28s n=%d count=%lld nonfinite=%lld max|x|=%.3e\n", what, n, (long long)count, (long long)bad, amax);
+  (void)ctx;
+}
+
 struct SvdOut {
   double* C = nullptr;
   double* Vk = nullptr;
@@ -763,7 +780,11 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     if (!pend.on) return;
     side_begin(ctx, sctx);  // after everything enqueued on main so far
     side_used = true;
+    dbg_nan(ctx, sctx.stream, "flush: Vk", pend.n, pend.so.Vk, (int64_t)pend.f2.b * pend.so.keep);
+    dbg_nan(ctx, sctx.stream, "flush: f2.T (tile 0)", pend.n, pend.f2.T, (int64_t)pend.f2.b * pend.f2.b);
+    dbg_nan(ctx, sctx.stream, "flush: f2.D", pend.n, pend.f2.D, pend.f2.b);
     tsqr_apply(sctx, pend.f2, pend.so.Vk, pend.so.keep, pend.out);
+    dbg_nan(ctx, sctx.stream, "flush: output core", pend.n, pend.out.base, pend.count);
     if (io) io->ready(pend.n, pend.out.base, pend.count, sctx.stream);
     ctx.free_after(pend.f2.mem, sctx.stream);  // returned to the pool on the main stream
     pend.f2.mem = nullptr;
@@ -778,7 +799,9 @@ static void round_impl(Ctx& ctx, int variant, double eps0, int64_t max_rank, int
     for (int n = N - 1; n >= 1; --n) {
       const int b = (int)r[n];
       Tsqr& f2 = f2cur;
+      dbg_nan(ctx, ctx.stream, "sweep2: panel in", n, out[n], r[n] * d[n] * r[n + 1]);
       { HostTimer ht("fac", &t_fac); tsqr_factor(ctx, panel_of(out[n], r[n], d[n], r[n + 1], 1), f2); }
+      dbg_nan(ctx, ctx.stream, "sweep2: R", n, f2.R, (int64_t)r[n] * r[n]);
       { HostTimer ht("flush", &t_flush); flush(); }  // previous step's output core overlaps this step's SVD
       SvdOut& so = socur;
       { HostTimer ht("svd", &t_svd); svd_of_rt(ctx, f2.R, b, eps, mr, so); }

@@ -435,13 +435,24 @@ __device__ void build_T(SM& sm, int b) {
 // [1, 2]); bv differs from beta only for an all-zero head column (v = e_j).
 // One rsqrt and one reciprocal, no divides.  Bitwise identical wherever it
 // is evaluated from the same (alpha, sig).
+// A column whose norm (pivot included) is below kTinyCol is treated as a zero
+// column: its squares sit in the underflow range, sig loses its bits (or is
+// flushed to an exact 0 while the entries are not), and 1 / (alpha - beta)
+// overflows -- a Householder vector of size 1e130 once put infinities into T
+// (LAPACK's dlarfg rescales such columns; here they only arise as roundoff of
+// roundoff on structurally rank-deficient bonds, 1e-140 of anything that
+// matters, so they are dropped: the reflector degenerates to a sign flip of
+// row j and the stored vector stays bounded).
+constexpr double kTinyCol = 1e-140;
+
 template <bool HEAD>
 __device__ __forceinline__ void reflector_scalars(double alpha, double sig, double& beta, double& tau, double& scal,
                                                   double& bv) {
-  if (sig == 0.0) {
+  const double n2 = fma(alpha, alpha, sig);
+  if (sig == 0.0 || n2 < kTinyCol * kTinyCol) {
     beta = -alpha;
     tau = 2.0;
-    if (HEAD && alpha == 0.0) {
+    if (HEAD && fabs(alpha) < kTinyCol) {
       scal = 1.0;
       bv = -1.0;
     } else {
@@ -449,7 +460,6 @@ __device__ __forceinline__ void reflector_scalars(double alpha, double sig, doub
       bv = beta;
     }
   } else {
-    const double n2 = fma(alpha, alpha, sig);
     const double rn = rsqrt(n2);
     const double nrm = n2 * rn;
     const double den = fabs(alpha) + nrm;

@@ -22,6 +22,13 @@ from oracle import tt_oracle as O  # noqa: E402
 TOL_TT = 1e-10
 TOL_SCALAR = 1e-12
 VARIANTS = ("LRLI", "RLRI", "LRL", "RLR")
+import os  # noqa: E402
+
+SEEDS = int(os.environ.get("TTB_SWEEP_SEEDS", "48"))  # a soak run sets a few hundred
+# seeds a 400-seed soak run failed on, kept as fixed cases: 234 (modes (2, 3, 618, 257, 257), ranks 64: roundoff
+# of roundoff on the rank-2 / rank-6 bonds put columns of norm ~1e-160 into a head tile; their squared norm
+# underflowed, the Householder vector overflowed and T went non-finite -- see kTinyCol in csrc/tsqr.cuh)
+SOAK_REGRESSIONS = [234]
 
 
 def dev(cores):
@@ -54,7 +61,7 @@ def chain(seed):
     return tuple(dims), tuple(ranks)
 
 
-@pytest.mark.parametrize("seed", range(48))
+@pytest.mark.parametrize("seed", sorted(set(range(SEEDS)) | set(SOAK_REGRESSIONS)))
 def test_random_chain_round_inner_norm(seed):
     dims, ranks = chain(seed)
     if seed % 5 == 4:  # a Hadamard product (ranks multiply: keep the factors <= 8)
