@@ -88,17 +88,19 @@ def test_random_chain_round_inner_norm(seed):
     assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant, eps)
     assert O.rel_diff(host(out), ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, variant, eps)
     # eps0 = 0 keeps every singular value that is not an exact zero, up to the
-    # cap.  On a bond whose rank is limited by a small mode (say 5 rows under a
-    # cap of 10) the surplus singular values are roundoff: LAPACK's gesdd
-    # returns them as tiny nonzeros, so the reference keeps them; the device
-    # Jacobi SVD deflates them to exact zeros and drops them (the same happens
-    # on the exactly dependent columns of X = Y + Y).  Ranks are therefore
-    # identical or smaller there, never larger, and the tensors agree.
+    # cap.  On a bond whose rank is limited by the structure (a small mode: say
+    # 5 rows under a cap of 10; the duplicated columns of Y + Y) the surplus
+    # singular values are roundoff, and whether one of them comes out as an
+    # exact zero or as 1e-17 depends on the SVD (LAPACK's gesdd in the
+    # reference, one-sided Jacobi with deflation on the device): a 1200-seed
+    # soak run saw the device keep fewer of them in most such cases and more
+    # in a few.  The ranks are compared where they carry information (every
+    # eps0 > 0 case above); here the results must be the same tensor within
+    # the cap.
     cap = max(1, max(O.ranks_of(x)) // 3)
     ref, _ = O.round_tt(x, 0.0, variant, cap)
     out = T.round_tt(dx, T.RoundingOptions(0.0, variant, max_rank=cap))
-    got_r, ref_r = tuple(out.ranks), O.ranks_of(ref)
-    assert all(g <= r for g, r in zip(got_r, ref_r)), (dims, ranks, variant, cap, got_r, ref_r)
+    assert max(out.ranks) <= cap, (dims, ranks, variant, cap, tuple(out.ranks))
     assert O.rel_diff(host(out), ref) < 1e-8, (dims, ranks, variant, cap)
 
 
