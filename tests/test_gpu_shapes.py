@@ -104,7 +104,7 @@ def test_random_chain_round_inner_norm(seed):
     assert O.rel_diff(host(out), ref) < 1e-8, (dims, ranks, variant, cap)
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(max(8, SEEDS // 6)))
 def test_random_chain_orthonormalize(seed):
     dims, ranks = chain(100 + seed)
     x = O.add(O.random_cores(dims, ranks, seed), O.random_cores(dims, ranks, seed + 7))
@@ -123,7 +123,7 @@ def test_random_chain_orthonormalize(seed):
             assert np.abs(g @ g - g).max() < 1e-10, (dims, ranks, direction, n)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(max(12, SEEDS // 4)))
 def test_random_chain_multirank(seed):
     """The same sweep through the native multi-rank path (in-process rank group,
     tests/test_gpu_multirank.py): P = 2, 3 or 4 ranks, idle ranks allowed where a
@@ -153,7 +153,7 @@ def test_random_chain_multirank(seed):
     assert O.rel_diff(res[0][1], ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, P, variant, eps)
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(max(8, SEEDS // 6)))
 def test_random_chain_wide_ranks(seed):
     """Bond ranks above 64 (the general path, csrc/wide.cu) on random chains:
     sums of two chains with ranks up to 70 each, and mixed chains where only
@@ -176,7 +176,7 @@ def test_random_chain_wide_ranks(seed):
     assert O.rel_diff(host(out), ref) < TOL_TT, (dims, ranks, variant)
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(max(6, SEEDS // 8)))
 def test_random_chain_round_hadamard(seed):
     """Implicit Hadamard-then-round (ops.py:109-132 then parallel.py:293) on
     random chains: ranks identical to rounding the materialised product by the
@@ -186,7 +186,7 @@ def test_random_chain_round_hadamard(seed):
     y = O.random_cores(dims, ranks, seed)
     w = O.random_cores(dims, ranks, seed + 77)
     variant = VARIANTS[seed % 4]
-    eps = float(10.0 ** -(4 + seed))
+    eps = float(10.0 ** -(4 + seed % 8))  # 1e-4 .. 1e-11: above the roundoff of the product
     ref, _ = O.round_tt(O.hadamard(y, w), eps, variant)
     out = T.round_hadamard(dev(y), dev(w), T.RoundingOptions(eps, variant))
     assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant, eps)
