@@ -191,3 +191,43 @@ def test_random_chain_round_hadamard(seed):
     out = T.round_hadamard(dev(y), dev(w), T.RoundingOptions(eps, variant))
     assert tuple(out.ranks) == O.ranks_of(ref), (dims, ranks, variant, eps)
     assert O.rel_diff(host(out), ref) < max(TOL_TT, 1e-3 * eps), (dims, ranks, variant, eps)
+
+
+@pytest.mark.parametrize("seed", range(max(10, SEEDS // 8)))
+def test_random_operator_apply(seed):
+    """Kronecker-operator apply (ops.py:314-342) on random chains and random
+    sparse factors (1 to 20 terms: the fused one-pass kernel takes up to 16,
+    more go term by term): bitwise the oracle's result, then apply + round."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.integers(1, 5))
+    dims = tuple(int(rng.integers(1, 90)) for _ in range(d))
+    ranks = (1,) + tuple(int(rng.integers(1, 7)) for _ in range(d - 1)) + (1,)
+    nterms = int(rng.choice([1, 2, 3, 8, 16, 17, 20]))
+    x = O.random_cores(dims, ranks, seed)
+    terms = []
+    for _ in range(nterms):
+        fac = []
+        for m in dims:
+            kind = rng.integers(0, 3)
+            if kind == 0:
+                a = sp.identity(m, format="csr")
+            elif kind == 1:
+                a = sp.diags([rng.standard_normal(m), rng.standard_normal(max(m - 1, 0))], [0, 1], shape=(m, m), format="csr")
+            else:
+                a = sp.random(m, m, density=min(1.0, 3.0 / m), random_state=int(rng.integers(1 << 30)), format="csr")
+            fac.append(sp.csr_matrix(a))
+        terms.append(fac)
+    op = T.KroneckerOperator(dims, terms)
+    want = O.apply_operator(op.terms, x)
+    z = T.apply_operator(op, T.TTTensor(x))
+    got = [c.array for c in z.cores]
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        assert a.shape == b.shape and np.array_equal(a, b), (dims, ranks, nterms)
+    if max(O.ranks_of(want)) <= 64:
+        ref, _ = O.round_tt(want, 1e-9, "LRLI")
+        zr = T.apply_operator(op, T.TTTensor(x), round_eps=1e-9)
+        assert tuple(zr.ranks) == O.ranks_of(ref), (dims, ranks, nterms)
+        assert O.rel_diff([c.array for c in zr.cores], ref) < TOL_TT, (dims, ranks, nterms)
