@@ -231,3 +231,30 @@ def test_random_operator_apply(seed):
         zr = T.apply_operator(op, T.TTTensor(x), round_eps=1e-9)
         assert tuple(zr.ranks) == O.ranks_of(ref), (dims, ranks, nterms)
         assert O.rel_diff([c.array for c in zr.cores], ref) < TOL_TT, (dims, ranks, nterms)
+
+
+@pytest.mark.parametrize("seed", range(max(16, SEEDS // 6)))
+def test_random_tsqr_blocks(seed):
+    """TSQR of random tall blocks across the chain / tree boundaries (one chain,
+    a few chains, one chain per SM, ragged last tiles; 1..64 columns): R against
+    numpy's QR (sign-fixed as tsqr.py:127-129), Q orthonormal, Q R = A, and the
+    implicit apply against the explicit Q."""
+    rng = np.random.default_rng(7000 + seed)
+    b = int(rng.choice([1, 2, 7, 15, 16, 17, 31, 32, 33, 48, 60, 63, 64]))
+    m = int(rng.choice([b, b + 1, 255, 256, 257, 511, 513, 1000, 4096, 4097, 20000, 37888, 37889, 75000, 151552]))
+    m = max(m, b)
+    a = rng.standard_normal((m, b))
+    if seed % 4 == 3:  # rank-deficient: duplicate the left half of the columns
+        a[:, b // 2:b // 2 + b // 2] = a[:, :b // 2]
+    fac, r = T.tsqr_factor(a)
+    q = T.tsqr_apply_q(fac, np.eye(b))
+    r_ref = np.linalg.qr(a, mode="r")
+    sgn = np.where(np.diag(r_ref) < 0, -1.0, 1.0)
+    r_ref = sgn[:, None] * r_ref
+    scale = np.abs(a).max() * np.sqrt(m)
+    assert np.abs(q.T @ q - np.eye(b)).max() < 1e-12, (m, b)
+    assert np.abs(q @ r - a).max() < 1e-12 * scale, (m, b)
+    if seed % 4 != 3:  # R is unique (up to the fixed signs) only at full rank
+        assert np.abs(r - r_ref).max() < 1e-11 * scale, (m, b)
+    c = rng.standard_normal((b, 5))
+    assert np.abs(T.tsqr_apply_q(fac, c) - q @ c).max() < 1e-11 * np.abs(c).max() * np.sqrt(b), (m, b)
